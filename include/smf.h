@@ -1,0 +1,172 @@
+/*
+ * smf.h -- C ABI of libsmf.so: the B200 (sm_100a) hot path of the sparse,
+ * albedo-corrected matched filter of Foote et al., "Fast and Accurate
+ * Retrieval of Methane Concentration from Imaging Spectrometer Data Using
+ * Sparsity Prior" (IEEE TGRS 2020, arXiv 2003.02978).
+ *
+ * Citations: P:n = line n of the paper text; "Fig. alg line k" =
+ * line k of its algorithm figure "AlbedoReWeightL1Filter".
+ *
+ * The operation (smf_retrieve) is the procedure AlbedoReWeightL1Filter(D, s,
+ * N_iter) run independently on every detector column of a radiance
+ * cube (one partition = one column):
+ *   mu0, C0 (lines 2-3) -> albedo r_i (line 5, Eq. 7) -> alpha0 (line 6, Eq. 3)
+ *   -> N_iter x { w (line 9, Eq. 5), mu^k, C^k (lines 10-14, Eq. 10-11),
+ *                 alpha^k = max((.)-w)/(r q), 0) (line 16, Eq. 6/8) }.
+ * The variant switches follow the figure's caption: sparsity off
+ * => w = 0; albedo off => r = 1. Readings of points the paper leaves open
+ * (clamping alpha0 before it feeds w^1/mu^1/C^1, the ridge, r floor, signed
+ * zero, 1/N) are listed in DESIGN.md section 2 and are the oracle's too.
+ *
+ * Conventions for every call:
+ *  - Every call returns smf_status; nothing throws or aborts across the ABI.
+ *  - Device pointers are CUDA device (or managed) memory owned by the CALLER;
+ *    the library never frees them. Host pointers are read during the call only.
+ *  - Layouts are C-contiguous: radiance [cols][pixels][bands] fp32 (column
+ *    major over detectors, pixels = along-track lines, bands contiguous);
+ *    enhancement / albedo [cols][pixels] fp32; column_status [cols] int32.
+ *  - Units: radiance arbitrary (the method is invariant to L -> cL);
+ *    s in (ppm m)^-1 (d ln L / d(ppm m), negative in absorption bands, P:119,
+ *    P:410); enhancement alpha in ppm m.
+ *  - stream is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Context threading: one retrieve in flight per (context, workspace) pair;
+ *    separate contexts are independent. A context binds to the CUDA device
+ *    current at smf_create.
+ */
+#ifndef SMF_H
+#define SMF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMF_ABI_VERSION 1
+
+typedef struct smf_ctx smf_ctx; /* opaque, library-owned (create/destroy) */
+
+typedef enum {
+    SMF_OK = 0,
+    SMF_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, bands < 1, cols < 1, pixels < 2,
+                                     n_iter < 0, eps <= 0, ridge < 0, r_floor <= 0,
+                                     aliasing outputs */
+    SMF_ERR_NOT_CONFIGURED = 2,   /* retrieve before smf_set_absorption */
+    SMF_ERR_SHAPE = 3,            /* bands != context bands, workspace too small,
+                                     or a shape this build does not support
+                                     (see smf_supported_bands) */
+    SMF_ERR_NUMERICAL = 4,        /* >= 1 column failed; per-column codes in column_status */
+    SMF_ERR_CUDA = 5,             /* CUDA runtime error; text via smf_last_error() */
+    SMF_ERR_OUT_OF_MEMORY = 6
+} smf_status;
+
+/* Per-column status codes written to column_status (device int32 [cols]). A
+ * failed column's enhancement and albedo are NaN; other columns are unaffected
+ * (cf. the paper skipping censored regions). */
+enum {
+    SMF_COL_OK = 0,
+    SMF_COL_NONFINITE = 1,         /* a non-finite radiance value in the column */
+    SMF_COL_DEGENERATE_MEAN = 2,   /* mu0 . mu0 = 0 with albedo correction (Eq. 7 undefined) */
+    SMF_COL_NOT_SPD = 3,           /* C^k + rho I not numerically positive definite */
+    SMF_COL_DEGENERATE_TARGET = 4  /* t^T (C^k+rho I)^-1 t <= 0 or non-finite (Eq. 3/6 undefined) */
+};
+
+/* Create a context for `bands` spectral bands on the current CUDA device.
+ * Defaults: eps = 1e-2 ppm m, ridge_rel = 0, r_floor = 0.05, n_iter = 30,
+ * sparsity and albedo correction on. *out = NULL on failure. */
+smf_status smf_create(smf_ctx** out, int bands);
+
+/* Destroy a context (NULL-safe). Does not touch caller-owned buffers. */
+void smf_destroy(smf_ctx* ctx);
+
+/* Set the unit absorption spectrum s (host fp32 [bands], copied). s is the
+ * per-band slope d ln L / d(ppm m); the target spectrum is
+ * t = mu (.) s (Eq. 9), recomputed from mu^k every iteration. */
+smf_status smf_set_absorption(smf_ctx* ctx, const float* s_host, int bands);
+
+/* Regularisation constants:
+ *  epsilon   > 0: the reweighting stabiliser of Eq. 5, w = 1/(alpha + eps);
+ *  ridge_rel >= 0: rho = ridge_rel * tr(C0)/bands, computed once per column from
+ *              C0 and added to every factored covariance (C0 and all C^k);
+ *              0 reproduces the paper's unregularised covariance;
+ *  r_floor   > 0: r~ = max(r, r_floor) wherever r enters the iteration
+ *              (denominator and signal removal); the raw r is reported. */
+smf_status smf_set_regularisation(smf_ctx* ctx, double epsilon, double ridge_rel, double r_floor);
+
+/* N_iter >= 0 (30 in the paper) and the Table I switches
+ * (P:389-391): use_sparsity = 0 enforces w = 0; use_albedo = 0
+ * sets r = 1. N_iter = 0 returns the unclamped closed form alpha0 (Eq. 3,
+ * divided by r~ when albedo correction is on). */
+smf_status smf_set_iterations(smf_ctx* ctx, int n_iter, int use_sparsity, int use_albedo);
+
+/* Device workspace bytes needed by smf_retrieve for this shape (host call). */
+smf_status smf_workspace_bytes(const smf_ctx* ctx, int cols, int pixels, size_t* bytes);
+
+/* Bands supported by this build: returns 1 if `bands` is supported, else 0. */
+int smf_supported_bands(int bands);
+
+/* The retrieval. Validates host-side arguments synchronously, enqueues every
+ * step on `stream` (all arithmetic in this library's CUDA kernels) and
+ * returns without synchronising.
+ *   radiance      device fp32 [cols][pixels][bands], read-only, 16-byte aligned
+ *   enhancement   device fp32 [cols][pixels] out: alpha^{N_iter} in ppm m
+ *   albedo        device fp32 [cols][pixels] out: raw r_i (Eq. 7), 1 if albedo off
+ *   workspace     device, >= smf_workspace_bytes(cols, pixels), 256-byte aligned
+ *   column_status device int32 [cols] out, or NULL
+ * enhancement and albedo must not alias each other or the radiance. */
+smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixels,
+                        float* enhancement, float* albedo, void* workspace,
+                        int32_t* column_status, void* stream);
+
+/* Wait for `stream`, then read `column_status` (device int32 [cols], as passed
+ * to smf_retrieve) and report the first failed column (-1 if none).
+ * Returns SMF_ERR_NUMERICAL if any column failed, SMF_ERR_CUDA on a CUDA error. */
+smf_status smf_synchronize(smf_ctx* ctx, void* stream, const int32_t* column_status, int cols,
+                           int* first_failed_column);
+
+/* End-to-end convenience call with HOST buffers (pinned or pageable):
+ * copies radiance host->device, runs smf_retrieve on an internal stream with
+ * context-owned device buffers (grown on demand and reused across calls),
+ * copies enhancement, albedo and column_status device->host and synchronises.
+ * Returns SMF_ERR_NUMERICAL if any column failed. */
+smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols, int pixels,
+                             float* enhancement_host, float* albedo_host,
+                             int32_t* column_status_host);
+
+/* Per-column background model after the last smf_retrieve that used
+ * `workspace`: mu^{N_iter} (device fp64 [cols][bands], or NULL) and
+ * q^{N_iter} = t^T (C+rho I)^-1 t (device fp64 [cols], or NULL). Enqueued on
+ * `stream`. */
+smf_status smf_column_model(smf_ctx* ctx, const void* workspace, int cols, int pixels,
+                            double* mu_out, double* q_out, void* stream);
+
+/* Initial statistics only (Fig. alg lines 2-3): mu0 (device fp64 [cols][bands])
+ * and C0 (device fp64 [cols][bands][bands], population 1/N covariance, no
+ * ridge), using the same statistics kernel as smf_retrieve. */
+smf_status smf_initial_statistics(smf_ctx* ctx, const float* radiance, int cols, int pixels,
+                                  double* mean_out, double* cov_out, void* workspace,
+                                  void* stream);
+
+/* Kernel launches enqueued by the last smf_retrieve call on this context. */
+int smf_last_launch_count(const smf_ctx* ctx);
+
+/* Per-kernel timing (measurement aid for bench.py): while enabled, every
+ * kernel launch of smf_retrieve is bracketed by two CUDA events recorded on
+ * the launching stream. smf_profile_enable(ctx, 1) also clears previous
+ * records. smf_profile_read synchronises on the recorded events and returns,
+ * for one kernel kind (SMF_KERNEL_*), the summed device duration in ms and
+ * the number of launches recorded since the last enable. */
+enum { SMF_KERNEL_STATS = 0, SMF_KERNEL_INIT = 1, SMF_KERNEL_UPDATE = 2, SMF_KERNEL_SWEEP = 3 };
+smf_status smf_profile_enable(smf_ctx* ctx, int enable);
+smf_status smf_profile_read(smf_ctx* ctx, int kernel_kind, double* total_ms, int* launches);
+
+const char* smf_status_string(smf_status status);
+const char* smf_last_error(const smf_ctx* ctx);
+int smf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMF_H */

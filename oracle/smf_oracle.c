@@ -73,12 +73,17 @@ void oracle_second_moment(int N, int B, const double* D, double* C) {
 }
 
 /* Lower Cholesky factor A = G G^T in place (lower triangle of A used).
- * Returns 0, or k+1 when pivot k is not positive / not finite. */
+ * Returns 0, or k+1 when pivot k is not numerically positive: not finite or
+ * <= n * 2^-52 * max_i A_ii (reading C16: a numerically singular covariance
+ * is reported as NOT_SPD instead of factored through a rounding-level pivot). */
 int oracle_cholesky(int n, double* A) {
+    double amax = 0.0;
+    for (int j = 0; j < n; ++j) amax = fmax(amax, A[(size_t)j * n + j]);
+    const double tol = (double)n * 2.220446049250313e-16 * amax;
     for (int j = 0; j < n; ++j) {
         double d = A[(size_t)j * n + j];
         for (int k = 0; k < j; ++k) d -= A[(size_t)j * n + k] * A[(size_t)j * n + k];
-        if (!(d > 0.0) || !isfinite(d)) return j + 1;
+        if (!(d > tol) || !isfinite(d)) return j + 1;
         double g = sqrt(d);
         A[(size_t)j * n + j] = g;
         for (int i = j + 1; i < n; ++i) {

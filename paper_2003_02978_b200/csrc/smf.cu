@@ -1,0 +1,662 @@
+// smf.cu -- C ABI of libsmf.so (include/smf.h): context, validation, workspace
+// layout, TMA descriptors and the launch sequence of the B200 hot path.
+//
+// Launch sequence of smf_retrieve (all on the caller's stream):
+//   K1 k1_stats (once)  -> K2 k2_init (once)  -> K3 k3_sweep(k=0)
+//   -> for k = 1..N_iter: K2 k2_update(k) -> K3 k3_sweep(k)
+// i.e. (N_iter + 2) passes over the radiance cube.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/smf.h"
+#include "kernels.cuh"
+
+using namespace smf;
+
+struct smf_ctx {
+    int device = 0;
+    int bands = 0;
+    int sm_count = 0;
+    float* s_dev = nullptr;
+    bool s_set = false;
+    double eps = 1e-2, ridge = 0.0, r_floor = 0.05;
+    int n_iter = 30, use_sparsity = 1, use_albedo = 1;
+    int last_launches = 0;
+    char err[512] = {0};
+    // profiling (smf_profile_*): events bracketing each launch
+    bool prof = false;
+    struct Rec { int kind; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    // smf_retrieve_host state
+    cudaStream_t h_stream = nullptr;
+    void* h_buf = nullptr;
+    size_t h_buf_bytes = 0;
+};
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+void load_encode() {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+}
+
+void set_err(smf_ctx* ctx, const char* fmt, ...) {
+    if (!ctx) return;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(ctx->err, sizeof(ctx->err), fmt, ap);
+    va_end(ap);
+}
+
+smf_status cuda_fail(smf_ctx* ctx, cudaError_t e, const char* where) {
+    set_err(ctx, "%s: %s", where, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? SMF_ERR_OUT_OF_MEMORY : SMF_ERR_CUDA;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+cudaEvent_t get_event(smf_ctx* ctx) {
+    if (!ctx->pool.empty()) {
+        cudaEvent_t e = ctx->pool.back();
+        ctx->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Bracket one launch with events when profiling is on.
+struct ProfScope {
+    smf_ctx* ctx;
+    cudaStream_t st;
+    int kind;
+    cudaEvent_t a = nullptr;
+    ProfScope(smf_ctx* c, cudaStream_t s, int k) : ctx(c), st(s), kind(k) {
+        if (ctx->prof) {
+            a = get_event(ctx);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (ctx->prof && a) {
+            cudaEvent_t b = get_event(ctx);
+            cudaEventRecord(b, st);
+            ctx->recs.push_back({kind, a, b});
+        }
+    }
+};
+
+// Static, balanced partition of the global tile stream (column-major tiles) over
+// the persistent sweep CTAs; S = max columns touched by one CTA.
+struct Plan {
+    int cols, N, B, tpc, G, S;
+    long long ttot;
+    // K1
+    int nblk, nb, G1, tiles_per_cta1, nch1;
+    size_t smem1, smem2, smem3;
+    // workspace offsets
+    size_t o_mbar, o_mu, o_tprev, o_yprev, o_ainv, o_q64, o_z32, o_mhat, o_kc, o_q32, o_status, o_pilot, o_part1,
+        o_part3, total;
+};
+
+int sweep_blocks_per_sm(int B);
+
+bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
+    const int B = ctx->bands;
+    p.cols = cols;
+    p.N = N;
+    p.B = B;
+    p.tpc = (N + kTileRows - 1) / kTileRows;
+    p.ttot = (long long)cols * p.tpc;
+    const int per_sm = std::max(1, sweep_blocks_per_sm(B));
+    long long G = (long long)ctx->sm_count * per_sm;
+    if (G > p.ttot) G = p.ttot;
+    p.G = (int)G;
+    int S = 1;
+    for (int b = 0; b < p.G; ++b) {
+        long long t0 = tile_begin(b, p.ttot, p.G), t1 = tile_begin(b + 1, p.ttot, p.G);
+        if (t1 > t0) S = std::max(S, (int)((t1 - 1) / p.tpc - t0 / p.tpc + 1));
+    }
+    p.S = S;
+    p.nblk = (B + 7) / 8;
+    p.nb = p.nblk * (p.nblk + 1) / 2;
+    p.G1 = 256 / p.nb;
+    p.tiles_per_cta1 = 32;
+    p.nch1 = (p.tpc + p.tiles_per_cta1 - 1) / p.tiles_per_cta1;
+    TileGeom g = TileGeom::make(B);
+    p.smem1 = k1_smem_bytes(B);
+    p.smem2 = k2_init_smem(B);
+    p.smem3 = (size_t)kStages * g.stage_bytes + 1024;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t r = o;
+        o = align_up(o + bytes, 256);
+        return r;
+    };
+    const size_t cb = (size_t)cols * B;
+    p.o_mbar = take(cb * 8);
+    p.o_mu = take(cb * 8);
+    p.o_tprev = take(cb * 8);
+    p.o_yprev = take(cb * 8);
+    p.o_ainv = take(cb * B * 8);
+    p.o_q64 = take((size_t)cols * 8);
+    p.o_z32 = take(cb * 4);
+    p.o_mhat = take(cb * 4);
+    p.o_kc = take((size_t)cols * 8);
+    p.o_q32 = take((size_t)cols * 4);
+    p.o_status = take((size_t)cols * 4);
+    p.o_pilot = take(cb * 4);
+    p.o_part1 = take((size_t)cols * p.nch1 * k1_width(p.nblk) * 8);
+    p.o_part3 = take((size_t)p.G * p.S * (B + 3) * 8);
+    p.total = o;
+    return true;
+}
+
+template <int NQ>
+void* sweep_fn() {
+    return reinterpret_cast<void*>(&k3_sweep<NQ>);
+}
+
+void* sweep_kernel(int B) {
+    switch (B / 4) {
+        case 1: return sweep_fn<1>();
+        case 2: return sweep_fn<2>();
+        case 3: return sweep_fn<3>();
+        case 4: return sweep_fn<4>();
+        case 5: return sweep_fn<5>();
+        case 6: return sweep_fn<6>();
+        case 7: return sweep_fn<7>();
+        case 8: return sweep_fn<8>();
+        case 9: return sweep_fn<9>();
+        case 10: return sweep_fn<10>();
+        case 11: return sweep_fn<11>();
+        case 12: return sweep_fn<12>();
+        case 13: return sweep_fn<13>();
+        case 14: return sweep_fn<14>();
+        case 15: return sweep_fn<15>();
+        case 16: return sweep_fn<16>();
+        case 17: return sweep_fn<17>();
+        case 18: return sweep_fn<18>();
+        case 19: return sweep_fn<19>();
+        case 20: return sweep_fn<20>();
+        case 21: return sweep_fn<21>();
+        case 22: return sweep_fn<22>();
+        case 23: return sweep_fn<23>();
+        case 24: return sweep_fn<24>();
+        default: return nullptr;
+    }
+}
+
+int sweep_blocks_per_sm(int B) {
+    void* fn = sweep_kernel(B);
+    if (!fn) return 0;
+    TileGeom g = TileGeom::make(B);
+    size_t smem = (size_t)kStages * g.stage_bytes + 1024;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kTileRows, smem) != cudaSuccess) return 1;
+    return std::max(n, 1);
+}
+
+bool supported(int B) { return B >= 4 && B <= 96 && B % 4 == 0; }
+
+CUresult make_maps(const float* rad, int cols, int N, int B, CUtensorMap* main_map, CUtensorMap* tail_map) {
+    TileGeom g = TileGeom::make(B);
+    cuuint64_t dims[3] = {(cuuint64_t)B, (cuuint64_t)N, (cuuint64_t)cols};
+    cuuint64_t strides[2] = {(cuuint64_t)B * 4, (cuuint64_t)N * B * 4};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = CUDA_SUCCESS;
+    memset(main_map, 0, sizeof(CUtensorMap));
+    memset(tail_map, 0, sizeof(CUtensorMap));
+    if (g.nfull > 0) {
+        cuuint32_t box[3] = {32, (cuuint32_t)kTileRows, 1};
+        r = g_encode(main_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)rad, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return r;
+    }
+    if (g.tailw > 0) {
+        cuuint32_t box[3] = {(cuuint32_t)g.tailw, (cuuint32_t)kTileRows, 1};
+        CUtensorMapSwizzle sw = g.tailw == 8 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                : g.tailw == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_128B;
+        r = g_encode(tail_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)rad, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    return r;
+}
+
+ColState col_state(const Plan& p, unsigned char* ws, const float* s) {
+    ColState cs;
+    cs.mbar = (double*)(ws + p.o_mbar);
+    cs.mu = (double*)(ws + p.o_mu);
+    cs.tprev = (double*)(ws + p.o_tprev);
+    cs.yprev = (double*)(ws + p.o_yprev);
+    cs.ainv = (double*)(ws + p.o_ainv);
+    cs.q64 = (double*)(ws + p.o_q64);
+    cs.z32 = (float*)(ws + p.o_z32);
+    cs.mhat32 = (float*)(ws + p.o_mhat);
+    cs.kc32 = (float*)(ws + p.o_kc);
+    cs.q32 = (float*)(ws + p.o_q32);
+    cs.status = (int*)(ws + p.o_status);
+    cs.s = s;
+    return cs;
+}
+
+smf_status validate(smf_ctx* ctx, const void* rad, int cols, int pixels, const void* ws) {
+    if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    if (!rad || !ws || cols < 1 || pixels < 2) {
+        set_err(ctx, "invalid argument (radiance/workspace NULL, cols < 1 or pixels < 2)");
+        return SMF_ERR_INVALID_ARGUMENT;
+    }
+    if (!ctx->s_set) {
+        set_err(ctx, "absorption spectrum not set (smf_set_absorption)");
+        return SMF_ERR_NOT_CONFIGURED;
+    }
+    if (((uintptr_t)rad & 15) || ((uintptr_t)ws & 255)) {
+        set_err(ctx, "radiance must be 16-byte and workspace 256-byte aligned");
+        return SMF_ERR_INVALID_ARGUMENT;
+    }
+    if (!g_encode) {
+        set_err(ctx, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+        return SMF_ERR_CUDA;
+    }
+    return SMF_OK;
+}
+
+// K1 + K2 init (shared by retrieve and initial_statistics)
+smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned char* ws, const CUtensorMap& mm,
+                        const CUtensorMap& tm, cudaStream_t st, double* mean_out, double* cov_out, int stats_only,
+                        int& launches) {
+    StatsArgs sa;
+    sa.L = rad;
+    sa.pilot = (float*)(ws + p.o_pilot);
+    sa.part1 = (double*)(ws + p.o_part1);
+    sa.cols = p.cols;
+    sa.N = p.N;
+    sa.B = p.B;
+    sa.tpc = p.tpc;
+    sa.nch1 = p.nch1;
+    sa.tiles_per_cta = p.tiles_per_cta1;
+    sa.nblk = p.nblk;
+    sa.nb = p.nb;
+    sa.G1 = p.G1;
+    cudaError_t e = cudaFuncSetAttribute(k1_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "k1_stats smem attribute");
+    {
+        ProfScope ps(ctx, st, SMF_KERNEL_STATS);
+        k1_stats<<<dim3(p.nch1, p.cols), 256, p.smem1, st>>>(mm, tm, sa);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "k1_stats launch");
+    ++launches;
+    InitArgs ia;
+    ia.cs = col_state(p, ws, ctx->s_dev);
+    ia.pilot = sa.pilot;
+    ia.part1 = sa.part1;
+    ia.mean_out = mean_out;
+    ia.cov_out = cov_out;
+    ia.cols = p.cols;
+    ia.N = p.N;
+    ia.B = p.B;
+    ia.nch1 = p.nch1;
+    ia.nblk = p.nblk;
+    ia.use_albedo = ctx->use_albedo;
+    ia.stats_only = stats_only;
+    ia.ridge_rel = ctx->ridge;
+    e = cudaFuncSetAttribute(k2_init, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem2);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "k2_init smem attribute");
+    {
+        ProfScope ps(ctx, st, SMF_KERNEL_INIT);
+        k2_init<<<p.cols, 256, p.smem2, st>>>(ia);
+    }
+    ++launches;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "k2_init launch");
+    return SMF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int smf_abi_version(void) { return SMF_ABI_VERSION; }
+
+int smf_supported_bands(int bands) { return supported(bands) ? 1 : 0; }
+
+const char* smf_status_string(smf_status s) {
+    switch (s) {
+        case SMF_OK: return "SMF_OK";
+        case SMF_ERR_INVALID_ARGUMENT: return "SMF_ERR_INVALID_ARGUMENT";
+        case SMF_ERR_NOT_CONFIGURED: return "SMF_ERR_NOT_CONFIGURED";
+        case SMF_ERR_SHAPE: return "SMF_ERR_SHAPE";
+        case SMF_ERR_NUMERICAL: return "SMF_ERR_NUMERICAL";
+        case SMF_ERR_CUDA: return "SMF_ERR_CUDA";
+        case SMF_ERR_OUT_OF_MEMORY: return "SMF_ERR_OUT_OF_MEMORY";
+    }
+    return "SMF_UNKNOWN";
+}
+
+const char* smf_last_error(const smf_ctx* ctx) { return ctx ? ctx->err : "NULL context"; }
+
+int smf_last_launch_count(const smf_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+smf_status smf_create(smf_ctx** out, int bands) {
+    if (!out) return SMF_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (bands < 1) return SMF_ERR_INVALID_ARGUMENT;
+    if (!supported(bands)) return SMF_ERR_SHAPE;
+    smf_ctx* ctx = new (std::nothrow) smf_ctx();
+    if (!ctx) return SMF_ERR_OUT_OF_MEMORY;
+    ctx->bands = bands;
+    cudaError_t e = cudaGetDevice(&ctx->device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, ctx->device);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->s_dev, sizeof(float) * bands);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return e == cudaErrorMemoryAllocation ? SMF_ERR_OUT_OF_MEMORY : SMF_ERR_CUDA;
+    }
+    std::call_once(g_encode_once, load_encode);
+    *out = ctx;
+    return SMF_OK;
+}
+
+smf_status smf_profile_enable(smf_ctx* ctx, int enable) {
+    if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    for (auto& r : ctx->recs) {
+        ctx->pool.push_back(r.a);
+        ctx->pool.push_back(r.b);
+    }
+    ctx->recs.clear();
+    ctx->prof = enable != 0;
+    return SMF_OK;
+}
+
+smf_status smf_profile_read(smf_ctx* ctx, int kind, double* total_ms, int* launches) {
+    if (!ctx || !total_ms || !launches) return SMF_ERR_INVALID_ARGUMENT;
+    double tot = 0.0;
+    int n = 0;
+    for (auto& r : ctx->recs) {
+        if (r.kind != kind) continue;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "profile_read");
+        tot += ms;
+        ++n;
+    }
+    *total_ms = tot;
+    *launches = n;
+    return SMF_OK;
+}
+
+void smf_destroy(smf_ctx* ctx) {
+    if (!ctx) return;
+    smf_profile_enable(ctx, 0);
+    for (auto e : ctx->pool) cudaEventDestroy(e);
+    cudaFree(ctx->s_dev);
+    if (ctx->h_buf) cudaFree(ctx->h_buf);
+    if (ctx->h_stream) cudaStreamDestroy(ctx->h_stream);
+    delete ctx;
+}
+
+smf_status smf_set_absorption(smf_ctx* ctx, const float* s_host, int bands) {
+    if (!ctx || !s_host) return SMF_ERR_INVALID_ARGUMENT;
+    if (bands != ctx->bands) {
+        set_err(ctx, "bands %d != context bands %d", bands, ctx->bands);
+        return SMF_ERR_SHAPE;
+    }
+    cudaError_t e = cudaMemcpy(ctx->s_dev, s_host, sizeof(float) * bands, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "set_absorption");
+    ctx->s_set = true;
+    return SMF_OK;
+}
+
+smf_status smf_set_regularisation(smf_ctx* ctx, double epsilon, double ridge_rel, double r_floor) {
+    if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    if (!(epsilon > 0.0) || !(ridge_rel >= 0.0) || !(r_floor > 0.0)) {
+        set_err(ctx, "need epsilon > 0, ridge_rel >= 0, r_floor > 0");
+        return SMF_ERR_INVALID_ARGUMENT;
+    }
+    ctx->eps = epsilon;
+    ctx->ridge = ridge_rel;
+    ctx->r_floor = r_floor;
+    return SMF_OK;
+}
+
+smf_status smf_set_iterations(smf_ctx* ctx, int n_iter, int use_sparsity, int use_albedo) {
+    if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    if (n_iter < 0) {
+        set_err(ctx, "n_iter < 0");
+        return SMF_ERR_INVALID_ARGUMENT;
+    }
+    ctx->n_iter = n_iter;
+    ctx->use_sparsity = use_sparsity ? 1 : 0;
+    ctx->use_albedo = use_albedo ? 1 : 0;
+    return SMF_OK;
+}
+
+smf_status smf_workspace_bytes(const smf_ctx* ctx, int cols, int pixels, size_t* bytes) {
+    if (!ctx || !bytes || cols < 1 || pixels < 2) return SMF_ERR_INVALID_ARGUMENT;
+    Plan p;
+    make_plan(ctx, cols, pixels, p);
+    *bytes = p.total;
+    return SMF_OK;
+}
+
+smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixels, float* enhancement,
+                        float* albedo, void* workspace, int32_t* column_status, void* stream) {
+    smf_status v = validate(ctx, radiance, cols, pixels, workspace);
+    if (v != SMF_OK) return v;
+    if (!enhancement || !albedo || (void*)enhancement == (void*)albedo ||
+        (void*)enhancement == (void*)radiance || (void*)albedo == (void*)radiance) {
+        set_err(ctx, "enhancement/albedo NULL or aliased");
+        return SMF_ERR_INVALID_ARGUMENT;
+    }
+    ctx->last_launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    Plan p;
+    make_plan(ctx, cols, pixels, p);
+    CUtensorMap mm, tm;
+    CUresult cr = make_maps(radiance, cols, pixels, ctx->bands, &mm, &tm);
+    if (cr != CUDA_SUCCESS) {
+        set_err(ctx, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+        return SMF_ERR_CUDA;
+    }
+    unsigned char* ws = (unsigned char*)workspace;
+    int launches = 0;
+    smf_status rc = launch_stats(ctx, p, radiance, ws, mm, tm, st, nullptr, nullptr, 0, launches);
+    if (rc != SMF_OK) return rc;
+    ColState cs = col_state(p, ws, ctx->s_dev);
+    SweepArgs sa;
+    sa.enh = enhancement;
+    sa.alb = albedo;
+    sa.z32 = cs.z32;
+    sa.mhat32 = cs.mhat32;
+    sa.kc32 = cs.kc32;
+    sa.q32 = cs.q32;
+    sa.status = cs.status;
+    sa.part3 = (double*)(ws + p.o_part3);
+    sa.cols = cols;
+    sa.N = pixels;
+    sa.B = p.B;
+    sa.tpc = p.tpc;
+    sa.G = p.G;
+    sa.S = p.S;
+    sa.ttot = p.ttot;
+    sa.n_iter = ctx->n_iter;
+    sa.use_sparsity = ctx->use_sparsity;
+    sa.use_albedo = ctx->use_albedo;
+    sa.eps = (float)ctx->eps;
+    sa.r_floor = (float)ctx->r_floor;
+    UpdateArgs ua;
+    ua.cs = cs;
+    ua.part3 = sa.part3;
+    ua.cols = cols;
+    ua.N = pixels;
+    ua.B = p.B;
+    ua.tpc = p.tpc;
+    ua.G = p.G;
+    ua.S = p.S;
+    ua.ttot = p.ttot;
+    void* kfn = sweep_kernel(p.B);
+    cudaError_t e0 = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem3);
+    if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k3_sweep smem attribute");
+    for (int k = 0; k <= ctx->n_iter; ++k) {
+        if (k > 0) {
+            {
+                ProfScope ps(ctx, st, SMF_KERNEL_UPDATE);
+                k2_update<<<cols, 128, 0, st>>>(ua);
+            }
+            e0 = cudaGetLastError();
+            if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k2_update launch");
+            ++launches;
+        }
+        sa.k = k;
+        void* args[] = {(void*)&mm, (void*)&tm, (void*)&sa};
+        cudaError_t e;
+        {
+            ProfScope ps(ctx, st, SMF_KERNEL_SWEEP);
+            e = cudaLaunchKernel(kfn, dim3(p.G), dim3(kTileRows), args, p.smem3, st);
+        }
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "sweep launch");
+        ++launches;
+    }
+    if (column_status) {
+        k_copy_status<<<(cols + 255) / 256, 256, 0, st>>>(cs.status, column_status, cols);
+        ++launches;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "retrieve launch");
+    ctx->last_launches = launches;
+    return SMF_OK;
+}
+
+smf_status smf_synchronize(smf_ctx* ctx, void* stream, const int32_t* column_status, int cols,
+                           int* first_failed_column) {
+    if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "synchronize");
+    if (first_failed_column) *first_failed_column = -1;
+    if (!column_status || cols < 1) return SMF_OK;
+    int32_t* h = new (std::nothrow) int32_t[cols];
+    if (!h) return SMF_ERR_OUT_OF_MEMORY;
+    e = cudaMemcpy(h, column_status, sizeof(int32_t) * cols, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+        delete[] h;
+        return cuda_fail(ctx, e, "synchronize status");
+    }
+    int first = -1;
+    for (int c = 0; c < cols && first < 0; ++c)
+        if (h[c] != SMF_COL_OK) first = c;
+    delete[] h;
+    if (first_failed_column) *first_failed_column = first;
+    if (first >= 0) {
+        set_err(ctx, "column %d failed", first);
+        return SMF_ERR_NUMERICAL;
+    }
+    return SMF_OK;
+}
+
+smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols, int pixels,
+                             float* enhancement_host, float* albedo_host, int32_t* column_status_host) {
+    if (!ctx || !radiance_host || !enhancement_host || !albedo_host || cols < 1 || pixels < 2)
+        return SMF_ERR_INVALID_ARGUMENT;
+    cudaError_t e;
+    if (!ctx->h_stream) {
+        e = cudaStreamCreateWithFlags(&ctx->h_stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "stream create");
+    }
+    size_t ws_bytes = 0;
+    smf_workspace_bytes(ctx, cols, pixels, &ws_bytes);
+    const size_t rad_bytes = align_up((size_t)cols * pixels * ctx->bands * 4, 256);
+    const size_t map_bytes = align_up((size_t)cols * pixels * 4, 256);
+    const size_t st_bytes = align_up((size_t)cols * 4, 256);
+    const size_t need = rad_bytes + 2 * map_bytes + st_bytes + ws_bytes;
+    if (need > ctx->h_buf_bytes) {
+        if (ctx->h_buf) cudaFree(ctx->h_buf);
+        ctx->h_buf = nullptr;
+        ctx->h_buf_bytes = 0;
+        e = cudaMalloc(&ctx->h_buf, need);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "retrieve_host alloc");
+        ctx->h_buf_bytes = need;
+    }
+    unsigned char* b = (unsigned char*)ctx->h_buf;
+    float* d_rad = (float*)b;
+    float* d_enh = (float*)(b + rad_bytes);
+    float* d_alb = (float*)(b + rad_bytes + map_bytes);
+    int32_t* d_st = (int32_t*)(b + rad_bytes + 2 * map_bytes);
+    void* d_ws = b + rad_bytes + 2 * map_bytes + st_bytes;
+    cudaStream_t st = ctx->h_stream;
+    e = cudaMemcpyAsync(d_rad, radiance_host, (size_t)cols * pixels * ctx->bands * 4, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D radiance");
+    smf_status rc = smf_retrieve(ctx, d_rad, cols, pixels, d_enh, d_alb, d_ws, d_st, st);
+    if (rc != SMF_OK) return rc;
+    e = cudaMemcpyAsync(enhancement_host, d_enh, (size_t)cols * pixels * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(albedo_host, d_alb, (size_t)cols * pixels * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && column_status_host)
+        e = cudaMemcpyAsync(column_status_host, d_st, (size_t)cols * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "retrieve_host D2H");
+    if (column_status_host)
+        for (int c = 0; c < cols; ++c)
+            if (column_status_host[c] != SMF_COL_OK) return SMF_ERR_NUMERICAL;
+    return SMF_OK;
+}
+
+smf_status smf_column_model(smf_ctx* ctx, const void* workspace, int cols, int pixels, double* mu_out,
+                            double* q_out, void* stream) {
+    if (!ctx || !workspace || cols < 1 || pixels < 2) return SMF_ERR_INVALID_ARGUMENT;
+    Plan p;
+    make_plan(ctx, cols, pixels, p);
+    const unsigned char* ws = (const unsigned char*)workspace;
+    ModelArgs a;
+    a.mu = (const double*)(ws + p.o_mu);
+    a.q64 = (const double*)(ws + p.o_q64);
+    a.mu_out = mu_out;
+    a.q_out = q_out;
+    a.cols = cols;
+    a.B = p.B;
+    int n = cols * p.B;
+    k_column_model<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "column_model");
+    return SMF_OK;
+}
+
+smf_status smf_initial_statistics(smf_ctx* ctx, const float* radiance, int cols, int pixels, double* mean_out,
+                                  double* cov_out, void* workspace, void* stream) {
+    smf_status v = validate(ctx, radiance, cols, pixels, workspace);
+    if (v != SMF_OK) return v;
+    Plan p;
+    make_plan(ctx, cols, pixels, p);
+    CUtensorMap mm, tm;
+    CUresult cr = make_maps(radiance, cols, pixels, ctx->bands, &mm, &tm);
+    if (cr != CUDA_SUCCESS) {
+        set_err(ctx, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+        return SMF_ERR_CUDA;
+    }
+    int launches = 0;
+    return launch_stats(ctx, p, radiance, (unsigned char*)workspace, mm, tm, (cudaStream_t)stream, mean_out, cov_out,
+                        1, launches);
+}
+
+}  // extern "C"
