@@ -76,31 +76,38 @@ __device__ __forceinline__ unsigned char* align1024(unsigned char* p) {
     return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-// ---------------------------------------------------------------- K1
-// Partial layout per (column, chunk), fp64, width k1_width(B):
-//   [nb][64]  sum x x^T per 8x8 block (lower triangle of blocks, row-major in block)
-//   [Bp]      sum x          (Bp = nblk*8)
-//   [Bp]      sum rho x
-//   [2]       sum rho, sum rho^2
-// with L - c = x + rho c (c = pilot mean of the first kPilotRows pixels).
-struct StatsArgs {
-    const float* L;      // radiance [cols][N][B]
-    float* pilot;        // [cols][B] pilot shift (written by chunk 0)
-    double* part1;       // [cols][nch1][k1_width]
-    int cols, N, B, tpc, nch1, tiles_per_cta, nblk, nb, G1;
+__host__ __device__ __forceinline__ long long tile_begin(long long b, long long ttot, int G) {
+    return b * ttot / G;
+}
+
+// Walks the column-major tile stream without a 64-bit division per tile.
+struct TileCursor {
+    int c, tt, tpc;
+    __device__ __forceinline__ TileCursor(long long g, int tpc_) : tpc(tpc_) {
+        c = (int)(g / tpc_);
+        tt = (int)(g - (long long)c * tpc_);
+    }
+    __device__ __forceinline__ void next() {
+        if (++tt == tpc) {
+            tt = 0;
+            ++c;
+        }
+    }
 };
 
-__host__ __device__ inline int k1_width(int nblk) { return nblk * (nblk + 1) / 2 * 64 + 2 * nblk * 8 + 2; }
-
-constexpr int kFlushTiles1 = 2;    // K1 fp32 run length: tiles between fp64 flushes
-
-// K1 dynamic smem: [kStages1 stages][64][NA] fp64 block accumulators
-// [G1*nblk][16] fp64 diagonal-thread band sums, NA = G1*nb active threads.
-__host__ __device__ inline size_t k1_smem_bytes(int B) {
-    const int nblk = (B + 7) / 8, nb = nblk * (nblk + 1) / 2, G1 = 256 / nb;
-    return (size_t)kStages1 * TileGeom::make(B).stage_bytes + (size_t)64 * G1 * nb * 8 +
-           (size_t)G1 * nblk * 16 * 8 + 1024;
-}
+// Shared-memory image of one TMA tile of ROWS pixels x 4*NQ bands (see TileGeom).
+template <int NQ, int ROWS = kTileRows>
+struct SweepGeom {
+    static constexpr int NFULL = NQ / 8;
+    static constexpr int TQ = NQ % 8;
+    static constexpr int TAILW = TQ == 0 ? 0 : (TQ <= 2 ? 8 : (TQ <= 4 ? 16 : 32));
+    static constexpr int STAGE = ((ROWS * (NFULL * 128 + TAILW * 4)) + 1023) / 1024 * 1024;
+    static constexpr uint32_t TX = ROWS * (NFULL * 128 + TAILW * 4);
+    static __device__ __forceinline__ uint32_t quad_off(int r, int q) {
+        if (q < NFULL * 8) return (q >> 3) * (ROWS * 128) + swz_off(r, q & 7, 128);
+        return NFULL * (ROWS * 128) + swz_off(r, q - NFULL * 8, TAILW * 4);
+    }
+};
 
 // Block (R, C) of the 8x8-blocked lower triangle, blk = R(R+1)/2 + C.
 __device__ __forceinline__ void blk_rc(int blk, int& R, int& C) {
@@ -110,186 +117,322 @@ __device__ __forceinline__ void blk_rc(int blk, int& R, int& C) {
     C = blk - r * (r + 1) / 2;
 }
 
-__global__ void __launch_bounds__(256, 1)
+// ---------------------------------------------------------------- K1
+// Extended-row SYRK. Each pixel row is shifted by the column's pilot mean c and
+// loses its component along c: sigma = L.ghat (ghat = c/|c|^2), x = L - sigma c,
+// rho = sigma - 1, so L - c = x + rho c exactly up to the rounding of x. The SYRK
+// runs on the extended row [x_0 .. x_{B-1}, rho, 1, 0, ...] (BE = round_up(B+2, 8)
+// bands), so one set of 8x8 register tiles yields sum x x^T, sum rho x, sum x,
+// sum rho^2, sum rho and N; K2 re-assembles mu0 and C0 from them in fp64.
+// The fp32 products are ~20x smaller than (L-c)(L-c)^T, fp32 runs last <= 16
+// tiles per thread and are then folded into an fp64 per-CTA buffer in a fixed
+// group order.
+//
+// Warp specialisation: NMW "main" warps own the 8x8 blocks (thread = (block,
+// row group g), rows g, g+G1, ...); one producer warp issues the TMA loads, reads
+// each landed (swizzled) tile and writes the extended rows into an unswizzled,
+// padded x-buffer (row stride odd in 16-byte units: conflict-free stores), one
+// tile ahead of the main warps. TMA ring: 2 stages (full barriers; the producer
+// refills a stage itself once it has read it). x ring: 2 stages (xready: 32
+// producer arrivals; xempty: NMW main-warp arrivals).
+constexpr int kFlush1 = 16;        // K1 tiles per fp32 run
+constexpr int kStagesK1 = 2;       // TMA ring depth
+constexpr int kMainWarps1 = 11;    // main-warp budget (12 warps with the producer: <= 170 regs)
+
+constexpr int k1_gcd(int a, int b) { return b == 0 ? a : k1_gcd(b, a % b); }
+
+template <int NQ>
+struct K1Geom {
+    static constexpr int B = NQ * 4;
+    static constexpr int BE = (B + 2 + 7) / 8 * 8;           // extended row (x, rho, 1, zeros)
+    static constexpr int NBLK = BE / 8;
+    static constexpr int NB = NBLK * (NBLK + 1) / 2;         // lower-triangle 8x8 blocks
+    static constexpr int G1r = (kMainWarps1 * 32) / NB;
+    static constexpr int G1 = G1r < 1 ? 1 : (G1r > kTileRows ? kTileRows : G1r);   // row groups
+    static constexpr int NA = G1 * NB;                       // active main threads
+    static constexpr int NMW = (NA + 31) / 32;               // main warps
+    static constexpr int NT = (NMW + 1) * 32;                // + producer warp
+    // tile height: a multiple of 32 (producer lanes) and of G1 (balanced groups) when <= 128
+    static constexpr int LCM = 32 / k1_gcd(32, G1) * G1;
+    static constexpr int T = LCM <= kTileRows ? LCM * (kTileRows / LCM) : kTileRows;
+    using Tile = SweepGeom<NQ, T>;
+    static constexpr int W = NB * 64;                        // partial width (fp64)
+    static constexpr int RQ = (BE / 4) % 2 == 0 ? BE / 4 + 1 : BE / 4;   // x row stride (quads, odd)
+    static constexpr int XSTAGE = (T * RQ * 16 + 1023) / 1024 * 1024;
+    static constexpr int RROWS = T / 32;                     // rows per producer lane
+    static constexpr size_t fixed_bytes = (size_t)2 * Tile::STAGE + (size_t)W * 8 + 1024;
+    static constexpr int XS = fixed_bytes + 3 * (size_t)XSTAGE <= 227 * 1024 ? 3
+                              : fixed_bytes + 2 * (size_t)XSTAGE <= 227 * 1024 ? 2 : 1;   // x ring depth
+};
+
+struct StatsArgs {
+    const float* pil32;    // [cols][B] pilot c
+    const float* ghat32;   // [cols][B] c/|c|^2
+    double* part1;         // [G1cta][S1][W]
+    int cols, N, B, tpc, G, S;
+    long long ttot;
+};
+
+template <int NQ>
+__host__ __device__ constexpr size_t k1_smem_bytes() {
+    using K = K1Geom<NQ>;
+    return (size_t)kStagesK1 * K1Geom<NQ>::Tile::STAGE + (size_t)K::XS * K::XSTAGE + (size_t)K::W * 8 + 1024;
+}
+
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(K1Geom<NQ>::NT, 1)
     k1_stats(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__ CUtensorMap tm_tail,
              StatsArgs a) {
+    using K = K1Geom<NQ>;
+    using Gm = typename K::Tile;
+    constexpr int B4 = NQ * 4;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char* stages = align1024(smem_raw);
-    __shared__ uint64_t full[kStages1];
-    __shared__ __align__(16) float pil[256];    // pilot c (zero-padded to nblk*8)
-    __shared__ __align__(16) float ghat[256];   // c / |c|^2
-    __shared__ float rho_s[kTileRows];
-    __shared__ double red_r[kTileRows * 2];
-    const TileGeom g = TileGeom::make(a.B);
-    const int NA = a.G1 * a.nb;                 // active threads
-    double* acc64 = reinterpret_cast<double*>(stages + kStages1 * g.stage_bytes);   // [64][NA]
-    double* dsum = acc64 + (size_t)64 * NA;    // [G1*nblk][16]: sum x (8), sum rho x (8)
-    const int tid = threadIdx.x;
-    const int c = blockIdx.y, j = blockIdx.x;
-    const int t0 = j * a.tiles_per_cta;
-    const int t1 = min(t0 + a.tiles_per_cta, a.tpc);
-    const int ntl = t1 - t0;
-    const int Bq = a.nblk * 2;   // quads covered by the blocks
+    const uint32_t raw = smem_u32(smem_raw);
+    unsigned char* stages = smem_raw + ((1024 - (raw & 1023)) & 1023);
+    const uint32_t stage0 = smem_u32(stages);
+    const uint32_t xb0 = stage0 + kStagesK1 * Gm::STAGE;
+    double* buf = reinterpret_cast<double*>(stages + kStagesK1 * Gm::STAGE + K::XS * K::XSTAGE);   // [NB][64]
+    __shared__ uint64_t full[kStagesK1], xready[K::XS], xempty[K::XS];
+    __shared__ __align__(16) float pil[B4];
+    __shared__ __align__(16) float gh[B4];
+
+    const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    const long long tb = tile_begin(blockIdx.x, a.ttot, a.G), te = tile_begin(blockIdx.x + 1, a.ttot, a.G);
+    const int ntl = (int)(te - tb);
+    const int cfirst = (int)(tb / a.tpc);
 
     if (tid == 0) {
-        for (int s = 0; s < kStages1; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < kStagesK1; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < K::XS; ++s) {
+            mbar_init(&xready[s], 32);
+            mbar_init(&xempty[s], K::NMW);
+        }
         fence_mbar_init();
-        for (int i = 0; i < kStages1 && i < ntl; ++i)
-            issue_tile(g, stages + i * g.stage_bytes, &full[i], &tm_main, &tm_tail, (t0 + i) * kTileRows, c);
     }
-    // pilot shift: fp32 mean of the first kPilotRows pixels, identical in every CTA
-    const int np = min(kPilotRows, a.N);
-    const size_t cbase = (size_t)c * a.N * a.B;
-    if (tid < a.nblk * 8) {
-        float sum = 0.f;
-        if (tid < a.B)
-            for (int p = 0; p < np; ++p) sum += a.L[cbase + (size_t)p * a.B + tid];
-        pil[tid] = tid < a.B ? sum / (float)np : 0.f;
-        if (j == 0 && tid < a.B) a.pilot[(size_t)c * a.B + tid] = pil[tid];
-    }
-    for (int i = tid; i < 64 * NA + a.G1 * a.nblk * 16; i += blockDim.x) acc64[i] = 0.0;
-    __syncthreads();
-    if (tid == 0) {
-        double cc = 0.0;
-        for (int b = 0; b < a.B; ++b) cc += (double)pil[b] * (double)pil[b];
-        red_r[0] = cc;
-    }
-    __syncthreads();
-    if (tid < a.nblk * 8) ghat[tid] = red_r[0] > 0.0 ? (float)((double)pil[tid] / red_r[0]) : 0.f;
+    for (int i = tid; i < K::W; i += K::NT) buf[i] = 0.0;
     __syncthreads();
 
-    const int blk = tid % a.nb, grp = tid / a.nb;
-    const bool active = grp < a.G1;
+    if (wid == K::NMW) {
+        // ===================== producer warp: TMA + extended-row rewrite =====================
+        TileCursor icur(tb, a.tpc);   // next tile to issue
+        auto issue = [&](int i) {
+            const int c = icur.c, row0 = icur.tt * K::T;
+            icur.next();
+            unsigned char* st = stages + (i % kStagesK1) * Gm::STAGE;
+            uint64_t* bar = &full[i % kStagesK1];
+            mbar_arrive_expect_tx(bar, Gm::TX);
+#pragma unroll
+            for (int f = 0; f < Gm::NFULL; ++f)
+                tma_load_3d(st + f * (K::T * 128), &tm_main, bar, f * 32, row0, c);
+            if (Gm::TAILW) tma_load_3d(st + Gm::NFULL * (K::T * 128), &tm_tail, bar, Gm::NFULL * 32, row0, c);
+        };
+        if (lane == 0) {
+            prefetch_tmap(&tm_main);
+            if (Gm::TAILW) prefetch_tmap(&tm_tail);
+            for (int i = 0; i < kStagesK1 && i < ntl; ++i) issue(i);
+        }
+        int cur = -1;
+        TileCursor ccur(tb, a.tpc);
+        // per-lane quad offsets: rows lane + 32 rr share (row & 7) and ((row >> 2) & 1)
+        uint32_t qo[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) qo[q] = Gm::quad_off(lane, q);
+        for (int i = 0; i < ntl; ++i, ccur.next()) {
+            const int c = ccur.c;
+            const int rowbase = ccur.tt * K::T;
+            if (c != cur) {
+                for (int b = lane; b < B4; b += 32) {
+                    pil[b] = a.pil32[(size_t)c * a.B + b];
+                    gh[b] = a.ghat32[(size_t)c * a.B + b];
+                }
+                __syncwarp();
+                cur = c;
+            }
+            const int s = i % kStagesK1, x = i % K::XS;
+            if (i >= K::XS) mbar_wait(&xempty[x], ((i - K::XS) / K::XS) & 1);   // main warps done with it
+            mbar_wait(&full[s], (i / kStagesK1) & 1);
+            const uint32_t sb = stage0 + s * Gm::STAGE;
+            const uint32_t xb = xb0 + x * K::XSTAGE;
+#pragma unroll 1
+            for (int rr = 0; rr < K::RROWS; ++rr) {
+                const int row = lane + 32 * rr;   // (row & 7) == (lane & 7)
+                const bool valid = rowbase + row < a.N;
+                float4 v[NQ];
+                float sgp[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const uint32_t rowoff = q < Gm::NFULL * 8 ? rr * 32 * 128 : rr * 32 * (Gm::TAILW * 4);
+                    v[q] = lds4(sb + qo[q] + rowoff);
+                }
+#pragma unroll
+                for (int q = 0; q < NQ; ++q)
+                    sgp[q & 3] = dot4(v[q], *reinterpret_cast<const float4*>(&gh[4 * q]), sgp[q & 3]);
+                const float sg = (sgp[0] + sgp[1]) + (sgp[2] + sgp[3]);
+                const uint32_t xr = xb + row * (K::RQ * 16);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const float4 cq = *reinterpret_cast<const float4*>(&pil[4 * q]);
+                    float4 xv;
+                    xv.x = fmaf(-sg, cq.x, v[q].x);
+                    xv.y = fmaf(-sg, cq.y, v[q].y);
+                    xv.z = fmaf(-sg, cq.z, v[q].z);
+                    xv.w = fmaf(-sg, cq.w, v[q].w);
+                    if (!valid) xv = make_float4(0.f, 0.f, 0.f, 0.f);
+                    sts4(xr + q * 16, xv);
+                }
+                sts4(xr + NQ * 16, valid ? make_float4(sg - 1.f, 1.f, 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f));
+#pragma unroll
+                for (int q = NQ + 1; q < K::BE / 4; ++q) sts4(xr + q * 16, make_float4(0.f, 0.f, 0.f, 0.f));
+            }
+            __syncwarp();
+            // TMA stage s has been read by every lane: refill it
+            if (lane == 0 && i + kStagesK1 < ntl) issue(i + kStagesK1);
+            mbar_arrive(&xready[x]);
+        }
+        return;
+    }
+
+    // ===================== main warps: 8x8 block outer products =====================
+    const bool active = tid < K::NA;
+    const int blk = tid % K::NB, grp = tid / K::NB;
     int R = 0, C = 0;
     blk_rc(blk, R, C);
-    const bool diag = R == C;
+    constexpr int RS = K::RQ * 16;   // x row stride (bytes)
+    constexpr int NMT = K::NMW * 32;
+    const int nrows = grp < K::T ? (K::T - grp + K::G1 - 1) / K::G1 : 0;
+
     float acc[64];
 #pragma unroll
     for (int i = 0; i < 64; ++i) acc[i] = 0.f;
-    double* dmine = dsum + (size_t)(grp * a.nblk + R) * 16;
-    float ms[8], mr[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ms[i] = mr[i] = 0.f;
-    double r1 = 0.0, r2 = 0.0;   // row owners: sum rho, sum rho^2
+    int run = 0;
 
-    for (int it = 0; it < ntl; ++it) {
-        const int s = it % kStages1;
-        mbar_wait(&full[s], (it / kStages1) & 1);
-        unsigned char* st = stages + s * g.stage_bytes;
-        const int rowbase = (t0 + it) * kTileRows;
-        // (1) rewrite the tile in place: x = (L - c) - rho c, rho = (L - c).ghat; rows >= N -> 0
-        if (tid < kTileRows) {
-            const bool valid = rowbase + tid < a.N;
-            float rho = 0.f;
-            for (int q = 0; q < Bq; ++q) {
-                float4 v = *reinterpret_cast<const float4*>(st + g.quad_off(tid, q));
-                const float4 cq = *reinterpret_cast<const float4*>(&pil[4 * q]);
-                const float4 gq = *reinterpret_cast<const float4*>(&ghat[4 * q]);
-                rho = fmaf(v.x - cq.x, gq.x, rho);
-                rho = fmaf(v.y - cq.y, gq.y, rho);
-                rho = fmaf(v.z - cq.z, gq.z, rho);
-                rho = fmaf(v.w - cq.w, gq.w, rho);
+    // fold the fp32 run into the fp64 buffer (fixed group order), optionally emit the column slot
+    auto fold = [&](bool emit, int slot) {
+        for (int q = 0; q < K::G1; ++q) {
+            if (active && grp == q) {
+#pragma unroll
+                for (int i = 0; i < 64; ++i) buf[blk * 64 + i] += (double)acc[i];
             }
-            if (!valid) rho = 0.f;
-            for (int q = 0; q < Bq; ++q) {
-                float4* pv = reinterpret_cast<float4*>(st + g.quad_off(tid, q));
-                float4 v = *pv;
-                const float4 cq = *reinterpret_cast<const float4*>(&pil[4 * q]);
-                float4 x;
-                x.x = fmaf(-rho, cq.x, v.x - cq.x);
-                x.y = fmaf(-rho, cq.y, v.y - cq.y);
-                x.z = fmaf(-rho, cq.z, v.z - cq.z);
-                x.w = fmaf(-rho, cq.w, v.w - cq.w);
-                if (!valid) x = make_float4(0.f, 0.f, 0.f, 0.f);
-                *pv = x;
-            }
-            rho_s[tid] = rho;
-            r1 += (double)rho;
-            r2 += (double)rho * (double)rho;
+            named_sync(1, NMT);
         }
-        __syncthreads();
-        // (2) 8x8 block outer products (fp32 run over this tile's rows)
+#pragma unroll
+        for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+        if (emit) {
+            double* out = a.part1 + ((size_t)blockIdx.x * a.S + slot) * K::W;
+            for (int i = tid; i < K::W; i += NMT) {
+                out[i] = buf[i];
+                buf[i] = 0.0;
+            }
+            named_sync(1, NMT);
+        }
+    };
+
+    int cur = -1;
+    TileCursor mcur(tb, a.tpc);
+    for (int it = 0; it < ntl; ++it, mcur.next()) {
+        const int c = mcur.c;
+        if (c != cur) {
+            if (cur >= 0) {
+                fold(true, cur - cfirst);
+                run = 0;
+            }
+            cur = c;
+        }
+        const int x = it % K::XS;
+        mbar_wait(&xready[x], (it / K::XS) & 1);
         if (active) {
-#pragma unroll 1
-            for (int r = grp; r < kTileRows; r += a.G1) {
-                const float4 a0 = *reinterpret_cast<const float4*>(st + g.quad_off(r, 2 * R));
-                const float4 a1 = *reinterpret_cast<const float4*>(st + g.quad_off(r, 2 * R + 1));
-                const float4 b0 = *reinterpret_cast<const float4*>(st + g.quad_off(r, 2 * C));
-                const float4 b1 = *reinterpret_cast<const float4*>(st + g.quad_off(r, 2 * C + 1));
+            uint32_t pa = xb0 + x * K::XSTAGE + grp * RS + R * 32;
+            uint32_t pb = xb0 + x * K::XSTAGE + grp * RS + C * 32;
+            // two register sets, rows k and k+1, so the loads of one row overlap the
+            // 64 FMAs of the other without register moves
+            auto rows8 = [&](const float4& a0, const float4& a1, const float4& b0, const float4& b1) {
                 const float xa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                const float xb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                const float xbv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) acc[i * 8 + k] = fmaf(xa[i], xb[k], acc[i * 8 + k]);
-                if (diag) {
-                    const float rho = rho_s[r];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        ms[i] += xa[i];
-                        mr[i] = fmaf(rho, xa[i], mr[i]);
-                    }
+                    for (int kk = 0; kk < 8; ++kk) acc[i * 8 + kk] = fmaf(xa[i], xbv[kk], acc[i * 8 + kk]);
+            };
+            constexpr uint32_t STEP = K::G1 * RS;
+            int k = 0;
+            float4 a0 = lds4(pa), a1 = lds4(pa + 16), b0 = lds4(pb), b1 = lds4(pb + 16);
+#pragma unroll 1
+            for (; k + 2 <= nrows; k += 2) {
+                const float4 c0 = lds4(pa + STEP), c1 = lds4(pa + STEP + 16);
+                const float4 d0 = lds4(pb + STEP), d1 = lds4(pb + STEP + 16);
+                rows8(a0, a1, b0, b1);
+                pa += 2 * STEP;
+                pb += 2 * STEP;
+                if (k + 2 < nrows) {
+                    a0 = lds4(pa);
+                    a1 = lds4(pa + 16);
+                    b0 = lds4(pb);
+                    b1 = lds4(pb + 16);
                 }
+                rows8(c0, c1, d0, d1);
             }
-            // (3) flush the fp32 run to fp64 every kFlushTiles1 tiles
-            if ((it + 1) % kFlushTiles1 == 0 || it + 1 == ntl) {
-#pragma unroll
-                for (int i = 0; i < 64; ++i) {
-                    acc64[(size_t)i * NA + tid] += (double)acc[i];
-                    acc[i] = 0.f;
-                }
-                if (diag) {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        dmine[i] += (double)ms[i];
-                        dmine[8 + i] += (double)mr[i];
-                        ms[i] = mr[i] = 0.f;
-                    }
-                }
-            }
+            if (k < nrows) rows8(a0, a1, b0, b1);
         }
-        __syncthreads();
-        if (tid == 0 && it + kStages1 < ntl)
-            issue_tile(g, stages + s * g.stage_bytes, &full[s], &tm_main, &tm_tail,
-                       (t0 + it + kStages1) * kTileRows, c);
-    }
-    __syncthreads();
-    // cross-group reduction in fixed group order
-    const int W1 = k1_width(a.nblk);
-    double* out = a.part1 + ((size_t)c * a.nch1 + j) * W1;
-    for (int e = tid; e < a.nb * 64; e += blockDim.x) {
-        const int b = e >> 6, i = e & 63;
-        double v = 0.0;
-        for (int q = 0; q < a.G1; ++q) v += acc64[(size_t)i * NA + q * a.nb + b];
-        out[e] = v;
-    }
-    // band sums from the diagonal-block threads, fixed group order
-    const int Bp = a.nblk * 8;
-    for (int b = tid; b < Bp; b += blockDim.x) {
-        double sx = 0.0, srx = 0.0;
-        for (int q = 0; q < a.G1; ++q) {
-            const double* d = dsum + (size_t)(q * a.nblk + (b >> 3)) * 16;
-            sx += d[b & 7];
-            srx += d[8 + (b & 7)];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty[x]);
+        if (++run == kFlush1) {
+            fold(false, 0);
+            run = 0;
         }
-        out[a.nb * 64 + b] = sx;
-        out[a.nb * 64 + Bp + b] = srx;
     }
-    // rho sums from the row owners, fixed order
-    if (tid < kTileRows) {
-        red_r[tid * 2] = r1;
-        red_r[tid * 2 + 1] = r2;
+    if (cur >= 0) fold(true, cur - cfirst);
+}
+
+// Pilot per column: c = fp32 mean of the first kPilotRows pixels, ghat = c/|c|^2.
+struct PilotArgs {
+    const float* L;
+    float* pil32;
+    float* ghat32;
+    int cols, N, B;
+};
+
+__global__ void k0_pilot(PilotArgs a) {
+    const int c = blockIdx.x, tid = threadIdx.x;
+    __shared__ double cc;
+    const int np = min(kPilotRows, a.N);
+    const size_t base = (size_t)c * a.N * a.B;
+    float v = 0.f;
+    if (tid < a.B) {
+        float sum = 0.f;
+        for (int p = 0; p < np; ++p) sum += a.L[base + (size_t)p * a.B + tid];
+        v = sum / (float)np;
+        a.pil32[(size_t)c * a.B + tid] = v;
     }
+    double sq[1] = {(double)v * (double)v};
+    __shared__ double scratch[32];
+    // block reduction (fixed order)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq[0] += __shfl_xor_sync(0xffffffffu, sq[0], off);
+    if ((tid & 31) == 0) scratch[tid >> 5] = sq[0];
     __syncthreads();
     if (tid == 0) {
-        double s1 = 0.0, s2 = 0.0;
-        for (int t = 0; t < kTileRows; ++t) {
-            s1 += red_r[t * 2];
-            s2 += red_r[t * 2 + 1];
-        }
-        out[a.nb * 64 + 2 * Bp] = s1;
-        out[a.nb * 64 + 2 * Bp + 1] = s2;
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t += scratch[w];
+        cc = t;
     }
+    __syncthreads();
+    if (tid < a.B) a.ghat32[(size_t)c * a.B + tid] = cc > 0.0 ? (float)((double)v / cc) : 0.f;
 }
 
 // ---------------------------------------------------------------- shared column state
@@ -332,21 +475,41 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch /* [3
 // ---------------------------------------------------------------- K2 init
 struct InitArgs {
     ColState cs;
-    const float* pilot;
-    const double* part1;
-    double* mean_out;   // optional [cols][B] (smf_initial_statistics)
-    double* cov_out;    // optional [cols][B][B]
-    int cols, N, B, nch1, nblk, use_albedo, stats_only;
+    const float* pil32;
+    const double* part1;   // K1 slots [G1][S1][W1]
+    double* mean_out;      // optional [cols][B] (smf_initial_statistics)
+    double* cov_out;       // optional [cols][B][B]
+    int cols, N, B, W1, tpc, G1, S1, use_albedo, stats_only;
+    long long ttot;
     double ridge_rel;
 };
 
-__host__ inline size_t k2_init_smem(int B) { return (size_t)B * B * 8 + 6 * (size_t)B * 8 + 32 * 4 * 8; }
+__host__ inline int k1_width_host(int B) {
+    const int nqe = B / 4 + 1, nblk = (nqe + 1) / 2;
+    return nblk * (nblk + 1) / 2 * 64;
+}
+
+__host__ inline size_t k2_init_smem(int B) {
+    return (size_t)B * B * 8 + (size_t)k1_width_host(B) * 8 + 6 * (size_t)B * 8 + 32 * 4 * 8;
+}
+
+// entry (i, k), i >= k, of the extended-row block sums
+__device__ __forceinline__ double ext_entry(const double* S, int i, int k) {
+    if (i < k) {
+        int t = i;
+        i = k;
+        k = t;
+    }
+    const int R = i >> 3, C = k >> 3;
+    return S[(R * (R + 1) / 2 + C) * 64 + (i & 7) * 8 + (k & 7)];
+}
 
 __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     extern __shared__ double sm2[];
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x;
     double* A = sm2;               // [B][B]
-    double* dm = A + B * B;        // [B] mean of L - c, later mu0
+    double* S = A + B * B;         // [W1] extended-row sums of this column
+    double* dm = S + a.W1;         // [B] mean of L - c, later mu0
     double* srx = dm + B;          // [B] sum rho x
     double* cv = srx + B;          // [B] pilot c
     double* rowj = cv + B;         // [B]
@@ -354,48 +517,52 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     double* vt = colj + B;         // [B] t0
     double* scratch = vt + B;      // [32][4]
     __shared__ int bad;
-    __shared__ double sh_tol, sh_mm, sh_r1, sh_r2;
-    const int nb = a.nblk * (a.nblk + 1) / 2, Bp = a.nblk * 8;
-    const int W1 = k1_width(a.nblk);
-    const double* P = a.part1 + (size_t)c * a.nch1 * W1;
+    __shared__ double sh_tol, sh_mm;
     const double invN = 1.0 / (double)a.N;
-    if (tid == 0) {
-        bad = COL_OK;
-        double s1 = 0.0, s2 = 0.0;
-        for (int j = 0; j < a.nch1; ++j) {
-            s1 += P[(size_t)j * W1 + nb * 64 + 2 * Bp];
-            s2 += P[(size_t)j * W1 + nb * 64 + 2 * Bp + 1];
+    // gather the K1 slots covering this column, fixed CTA order
+    {
+        const long long c0 = (long long)c * a.tpc, c1 = c0 + a.tpc;
+        int b0 = (int)((c0 * a.G1) / a.ttot);
+        while (b0 > 0 && tile_begin(b0, a.ttot, a.G1) > c0) --b0;
+        while (tile_begin(b0 + 1, a.ttot, a.G1) <= c0) ++b0;
+        for (int i = tid; i < a.W1; i += blockDim.x) {
+            double v = 0.0;
+            for (int b = b0; b < a.G1 && tile_begin(b, a.ttot, a.G1) < c1; ++b) {
+                const int slot = c - (int)(tile_begin(b, a.ttot, a.G1) / a.tpc);
+                v += a.part1[((size_t)b * a.S1 + slot) * a.W1 + i];
+            }
+            S[i] = v;
         }
-        sh_r1 = s1;
-        sh_r2 = s2;
     }
+    if (tid == 0) bad = COL_OK;
     __syncthreads();
+    const double Sr = ext_entry(S, B + 1, B), Srr = ext_entry(S, B, B);
     // sum (L - c) = sum x + (sum rho) c ;  dm = mean(L) - c
     for (int b = tid; b < B; b += blockDim.x) {
-        double sx = 0.0, sr = 0.0;
-        for (int j = 0; j < a.nch1; ++j) {
-            sx += P[(size_t)j * W1 + nb * 64 + b];
-            sr += P[(size_t)j * W1 + nb * 64 + Bp + b];
-        }
-        cv[b] = (double)a.pilot[(size_t)c * B + b];
-        srx[b] = sr;
-        dm[b] = (sx + sh_r1 * cv[b]) * invN;
+        cv[b] = (double)a.pil32[(size_t)c * B + b];
+        srx[b] = ext_entry(S, B, b);
+        dm[b] = (ext_entry(S, B + 1, b) + Sr * cv[b]) * invN;
     }
     __syncthreads();
     // sum (L-c)(L-c)^T = Sxx + Srx c^T + c Srx^T + Srr c c^T ;  C0 = that/N - dm dm^T
     int nonfinite = 0;
-    for (int e = tid; e < B * B; e += blockDim.x) {
-        int i = e / B, k = e % B;
-        if (i < k) continue;
-        int R = i >> 3, C = k >> 3;
-        int off = (R * (R + 1) / 2 + C) * 64 + (i & 7) * 8 + (k & 7);
-        double sxx = 0.0;
-        for (int j = 0; j < a.nch1; ++j) sxx += P[(size_t)j * W1 + off];
-        double s2 = sxx + srx[i] * cv[k] + cv[i] * srx[k] + sh_r2 * cv[i] * cv[k];
-        double v = s2 * invN - dm[i] * dm[k];
+    // (i, k) walk over the B x B entries without integer division in the loop
+    const int i0 = tid / B, k0 = tid % B, di = blockDim.x / B, dk = blockDim.x % B;
+    for (int i = i0, k = k0; i < B;) {
+        const int ci = i, ck = k;
+        k += dk;
+        i += di;
+        if (k >= B) {
+            k -= B;
+            ++i;
+        }
+        if (ci < ck) continue;
+        const int ii = ci, kk = ck;
+        double s2 = ext_entry(S, ii, kk) + srx[ii] * cv[kk] + cv[ii] * srx[kk] + Srr * cv[ii] * cv[kk];
+        double v = s2 * invN - dm[ii] * dm[kk];
         if (!isfinite(v)) nonfinite = 1;
-        A[i * B + k] = v;
-        A[k * B + i] = v;
+        A[ii * B + kk] = v;
+        A[kk * B + ii] = v;
     }
     for (int b = tid; b < B; b += blockDim.x)
         if (!isfinite(dm[b])) nonfinite = 1;
@@ -434,7 +601,9 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     }
     __syncthreads();
     // in-place Gauss-Jordan inverse of the SPD matrix A = C0 + rho I (no pivoting;
-    // pivot j equals the j-th Cholesky pivot squared, checked like the oracle's)
+    // pivot j equals the j-th Cholesky pivot squared, checked like the oracle's).
+    // Thread (ty, tx) = (tid / 32, tid % 32) owns rows ty + 8m, columns tx + 32n.
+    const int tx = tid & 31, ty = tid >> 5;
     for (int j = 0; j < B && bad == COL_OK; ++j) {
         for (int k = tid; k < B; k += blockDim.x) {
             rowj[k] = A[j * B + k];
@@ -448,15 +617,19 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
             break;
         }
         const double p = 1.0 / piv;
-        for (int e = tid; e < B * B; e += blockDim.x) {
-            int i = e / B, k = e % B;
-            double v;
-            if (i == j && k == j) v = p;
-            else if (i == j) v = rowj[k] * p;
-            else if (k == j) v = -colj[i] * p;
-            else v = A[e] - colj[i] * rowj[k] * p;
-            A[e] = v;
+        for (int i = ty; i < B; i += 8) {
+            const double ci = colj[i] * p;
+            double* Ai = A + i * B;
+            for (int k = tx; k < B; k += 32) Ai[k] = fma(-ci, rowj[k], Ai[k]);
         }
+        __syncthreads();
+        // row j, column j, pivot
+        for (int k = tid; k < B; k += blockDim.x) {
+            A[j * B + k] = rowj[k] * p;
+            A[k * B + j] = -colj[k] * p;
+        }
+        __syncthreads();
+        if (tid == 0) A[j * B + j] = p;
         __syncthreads();
     }
     int st = bad;
@@ -505,9 +678,6 @@ struct UpdateArgs {
     long long ttot;
 };
 
-__host__ __device__ __forceinline__ long long tile_begin(long long b, long long ttot, int G) {
-    return b * ttot / G;
-}
 
 // Solve the 3x3 system K x = v by Gaussian elimination with partial pivoting.
 __device__ __forceinline__ bool solve3(double K[3][3], double v[3], double x[3]) {
@@ -542,6 +712,8 @@ __device__ __forceinline__ bool solve3(double K[3][3], double v[3], double x[3])
 
 __global__ void __launch_bounds__(128) k2_update(UpdateArgs a) {
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x;
+    extern __shared__ double sAinv[];   // [B][B] A^-1 of this column (bulk copy)
+    __shared__ uint64_t abar;
     __shared__ double sh_t[128], sh_h[128];
     __shared__ double scratch[32 * 9];
     __shared__ double sh_coef[3];
@@ -550,6 +722,15 @@ __global__ void __launch_bounds__(128) k2_update(UpdateArgs a) {
     ColState& cs = a.cs;
     const int st0 = cs.status[c];
     if (st0 != COL_OK) return;   // uniform per block
+    if (tid == 0) {
+        // stream A^-1 (41 KB at B = 72) into smem with one TMA bulk copy while the
+        // partials are reduced
+        mbar_init(&abar, 1);
+        fence_mbar_init();
+        const uint32_t bytes = (uint32_t)B * B * 8;
+        mbar_arrive_expect_tx(&abar, bytes);
+        bulk_load(sAinv, cs.ainv + (size_t)c * B * B, bytes, &abar);
+    }
     // 1. sufficient statistics of sweep k-1 (fixed CTA order)
     const long long c0 = (long long)c * a.tpc, c1 = c0 + a.tpc;
     int b0 = (int)((c0 * a.G) / a.ttot);
@@ -592,11 +773,12 @@ __global__ void __launch_bounds__(128) k2_update(UpdateArgs a) {
     __syncthreads();
     // 2. y_t = A^-1 t, y_h = A^-1 h  (A^-1 symmetric: row i, column = tid -> coalesced)
     double yt = 0.0, yh = 0.0;
+    mbar_wait(&abar, 0);
     if (tid < B) {
-        const double* Ai = cs.ainv + (size_t)c * B * B + tid;
+        const double* Ai = sAinv + tid;
 #pragma unroll 8
         for (int i = 0; i < B; ++i) {
-            const double v = Ai[(size_t)i * B];
+            const double v = Ai[i * B];
             yt = fma(v, sh_t[i], yt);
             yh = fma(v, sh_h[i], yh);
         }
@@ -679,19 +861,6 @@ struct SweepArgs {
 };
 
 template <int NQ>
-struct SweepGeom {
-    static constexpr int NFULL = NQ / 8;
-    static constexpr int TQ = NQ % 8;
-    static constexpr int TAILW = TQ == 0 ? 0 : (TQ <= 2 ? 8 : (TQ <= 4 ? 16 : 32));
-    static constexpr int STAGE = ((kTileRows * (NFULL * 128 + TAILW * 4)) + 1023) / 1024 * 1024;
-    static constexpr uint32_t TX = kTileRows * (NFULL * 128 + TAILW * 4);
-    static __device__ __forceinline__ uint32_t quad_off(int r, int q) {
-        if (q < NFULL * 8) return (q >> 3) * (kTileRows * 128) + swz_off(r, q & 7, 128);
-        return NFULL * (kTileRows * 128) + swz_off(r, q - NFULL * 8, TAILW * 4);
-    }
-};
-
-template <int NQ>
 __global__ void __launch_bounds__(kTileRows, 2)
     k3_sweep(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__ CUtensorMap tm_tail,
              SweepArgs a) {
@@ -720,9 +889,10 @@ __global__ void __launch_bounds__(kTileRows, 2)
         fence_mbar_init();
     }
     __syncthreads();
+    TileCursor icur(tb, a.tpc);   // next tile to issue (thread 0 only)
     auto issue = [&](int i) {
-        const long long g = tb + i;
-        const int c = (int)(g / a.tpc), row0 = (int)(g % a.tpc) * kTileRows;
+        const int c = icur.c, row0 = icur.tt * kTileRows;
+        icur.next();
         unsigned char* st = stages + (i % kStages) * Gm::STAGE;
         uint64_t* bar = &full[i % kStages];
         mbar_arrive_expect_tx(bar, Gm::TX);
@@ -776,10 +946,10 @@ __global__ void __launch_bounds__(kTileRows, 2)
     int cur = -1;
     float mz = 0.f, cz = 0.f, q = 1.f, mmf = 1.f;
     int cst = 0;
-    for (int i = 0; i < ntl; ++i) {
-        const long long g = tb + i;
-        const int c = (int)(g / a.tpc);
-        const int row0 = (int)(g % a.tpc) * kTileRows;
+    TileCursor ccur(tb, a.tpc);
+    for (int i = 0; i < ntl; ++i, ccur.next()) {
+        const int c = ccur.c;
+        const int row0 = ccur.tt * kTileRows;
         if (c != cur) {
             if (cur >= 0 && accum) flush(cur - cfirst);
             if (tid < B4) {

@@ -107,15 +107,18 @@ struct ProfScope {
 struct Plan {
     int cols, N, B, tpc, G, S;
     long long ttot;
-    // K1
-    int nblk, nb, G1, tiles_per_cta1, nch1;
+    // K1 (persistent, one CTA per SM, own tile height T1 and partition)
+    int G1, S1, W1, T1, tpc1;
+    long long ttot1;
     size_t smem1, smem2, smem3;
     // workspace offsets
-    size_t o_mbar, o_mu, o_tprev, o_yprev, o_ainv, o_q64, o_z32, o_mhat, o_kc, o_q32, o_status, o_pilot, o_part1,
+    size_t o_mbar, o_mu, o_tprev, o_yprev, o_ainv, o_q64, o_z32, o_mhat, o_kc, o_q32, o_status, o_pilot, o_ghat, o_part1,
         o_part3, total;
 };
 
 int sweep_blocks_per_sm(int B);
+size_t k1_smem(int B);
+int k1_rows(int B);
 
 bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     const int B = ctx->bands;
@@ -134,13 +137,18 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
         if (t1 > t0) S = std::max(S, (int)((t1 - 1) / p.tpc - t0 / p.tpc + 1));
     }
     p.S = S;
-    p.nblk = (B + 7) / 8;
-    p.nb = p.nblk * (p.nblk + 1) / 2;
-    p.G1 = 256 / p.nb;
-    p.tiles_per_cta1 = 32;
-    p.nch1 = (p.tpc + p.tiles_per_cta1 - 1) / p.tiles_per_cta1;
+    p.T1 = k1_rows(B);
+    p.tpc1 = (N + p.T1 - 1) / p.T1;
+    p.ttot1 = (long long)cols * p.tpc1;
+    p.G1 = (int)std::min<long long>(ctx->sm_count, p.ttot1);
+    p.S1 = 1;
+    for (int b = 0; b < p.G1; ++b) {
+        long long t0 = tile_begin(b, p.ttot1, p.G1), t1 = tile_begin(b + 1, p.ttot1, p.G1);
+        if (t1 > t0) p.S1 = std::max(p.S1, (int)((t1 - 1) / p.tpc1 - t0 / p.tpc1 + 1));
+    }
+    p.W1 = k1_width_host(B);
     TileGeom g = TileGeom::make(B);
-    p.smem1 = k1_smem_bytes(B);
+    p.smem1 = k1_smem(B);
     p.smem2 = k2_init_smem(B);
     p.smem3 = (size_t)kStages * g.stage_bytes + 1024;
     size_t o = 0;
@@ -162,7 +170,8 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.o_q32 = take((size_t)cols * 4);
     p.o_status = take((size_t)cols * 4);
     p.o_pilot = take(cb * 4);
-    p.o_part1 = take((size_t)cols * p.nch1 * k1_width(p.nblk) * 8);
+    p.o_ghat = take(cb * 4);
+    p.o_part1 = take((size_t)p.G1 * p.S1 * p.W1 * 8);
     p.o_part3 = take((size_t)p.G * p.S * (B + 3) * 8);
     p.total = o;
     return true;
@@ -203,6 +212,60 @@ void* sweep_kernel(int B) {
     }
 }
 
+template <int NQ>
+void* stats_fn() {
+    return reinterpret_cast<void*>(&k1_stats<NQ>);
+}
+
+template <int NQ>
+size_t stats_smem() {
+    return k1_smem_bytes<NQ>();
+}
+
+#define SMF_NQ_CASES(M) \
+    M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16) M(17) M(18) M(19) \
+        M(20) M(21) M(22) M(23) M(24)
+
+void* stats_kernel(int B) {
+    switch (B / 4) {
+#define SMF_CASE(n) \
+    case n: return stats_fn<n>();
+        SMF_NQ_CASES(SMF_CASE)
+#undef SMF_CASE
+        default: return nullptr;
+    }
+}
+
+int k1_rows(int B) {
+    switch (B / 4) {
+#define SMF_CASE(n) \
+    case n: return K1Geom<n>::T;
+        SMF_NQ_CASES(SMF_CASE)
+#undef SMF_CASE
+        default: return kTileRows;
+    }
+}
+
+int stats_threads(int B) {
+    switch (B / 4) {
+#define SMF_CASE(n) \
+    case n: return K1Geom<n>::NT;
+        SMF_NQ_CASES(SMF_CASE)
+#undef SMF_CASE
+        default: return 0;
+    }
+}
+
+size_t k1_smem(int B) {
+    switch (B / 4) {
+#define SMF_CASE(n) \
+    case n: return stats_smem<n>();
+        SMF_NQ_CASES(SMF_CASE)
+#undef SMF_CASE
+        default: return 0;
+    }
+}
+
 int sweep_blocks_per_sm(int B) {
     void* fn = sweep_kernel(B);
     if (!fn) return 0;
@@ -216,7 +279,8 @@ int sweep_blocks_per_sm(int B) {
 
 bool supported(int B) { return B >= 4 && B <= 96 && B % 4 == 0; }
 
-CUresult make_maps(const float* rad, int cols, int N, int B, CUtensorMap* main_map, CUtensorMap* tail_map) {
+CUresult make_maps(const float* rad, int cols, int N, int B, CUtensorMap* main_map, CUtensorMap* tail_map,
+                   int rows = kTileRows) {
     TileGeom g = TileGeom::make(B);
     cuuint64_t dims[3] = {(cuuint64_t)B, (cuuint64_t)N, (cuuint64_t)cols};
     cuuint64_t strides[2] = {(cuuint64_t)B * 4, (cuuint64_t)N * B * 4};
@@ -225,14 +289,14 @@ CUresult make_maps(const float* rad, int cols, int N, int B, CUtensorMap* main_m
     memset(main_map, 0, sizeof(CUtensorMap));
     memset(tail_map, 0, sizeof(CUtensorMap));
     if (g.nfull > 0) {
-        cuuint32_t box[3] = {32, (cuuint32_t)kTileRows, 1};
+        cuuint32_t box[3] = {32, (cuuint32_t)rows, 1};
         r = g_encode(main_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)rad, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return r;
     }
     if (g.tailw > 0) {
-        cuuint32_t box[3] = {(cuuint32_t)g.tailw, (cuuint32_t)kTileRows, 1};
+        cuuint32_t box[3] = {(cuuint32_t)g.tailw, (cuuint32_t)rows, 1};
         CUtensorMapSwizzle sw = g.tailw == 8 ? CU_TENSOR_MAP_SWIZZLE_32B
                                 : g.tailw == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                 : CU_TENSOR_MAP_SWIZZLE_128B;
@@ -281,43 +345,64 @@ smf_status validate(smf_ctx* ctx, const void* rad, int cols, int pixels, const v
     return SMF_OK;
 }
 
-// K1 + K2 init (shared by retrieve and initial_statistics)
-smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned char* ws, const CUtensorMap& mm,
-                        const CUtensorMap& tm, cudaStream_t st, double* mean_out, double* cov_out, int stats_only,
-                        int& launches) {
+// K0 pilot + K1 stats + K2 init (shared by retrieve and initial_statistics)
+smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned char* ws, cudaStream_t st,
+                        double* mean_out, double* cov_out, int stats_only, int& launches) {
+    CUtensorMap mm, tm;
+    CUresult cr = make_maps(rad, p.cols, p.N, p.B, &mm, &tm, p.T1);
+    if (cr != CUDA_SUCCESS) {
+        set_err(ctx, "cuTensorMapEncodeTiled (K1) failed (%d)", (int)cr);
+        return SMF_ERR_CUDA;
+    }
+    PilotArgs pa;
+    pa.L = rad;
+    pa.pil32 = (float*)(ws + p.o_pilot);
+    pa.ghat32 = (float*)(ws + p.o_ghat);
+    pa.cols = p.cols;
+    pa.N = p.N;
+    pa.B = p.B;
+    {
+        ProfScope ps(ctx, st, SMF_KERNEL_STATS);
+        k0_pilot<<<p.cols, 128, 0, st>>>(pa);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "k0_pilot launch");
+    ++launches;
     StatsArgs sa;
-    sa.L = rad;
-    sa.pilot = (float*)(ws + p.o_pilot);
+    sa.pil32 = pa.pil32;
+    sa.ghat32 = pa.ghat32;
     sa.part1 = (double*)(ws + p.o_part1);
     sa.cols = p.cols;
     sa.N = p.N;
     sa.B = p.B;
-    sa.tpc = p.tpc;
-    sa.nch1 = p.nch1;
-    sa.tiles_per_cta = p.tiles_per_cta1;
-    sa.nblk = p.nblk;
-    sa.nb = p.nb;
-    sa.G1 = p.G1;
-    cudaError_t e = cudaFuncSetAttribute(k1_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
+    sa.tpc = p.tpc1;
+    sa.G = p.G1;
+    sa.S = p.S1;
+    sa.ttot = p.ttot1;
+    void* k1 = stats_kernel(p.B);
+    e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k1_stats smem attribute");
     {
         ProfScope ps(ctx, st, SMF_KERNEL_STATS);
-        k1_stats<<<dim3(p.nch1, p.cols), 256, p.smem1, st>>>(mm, tm, sa);
+        void* args[] = {(void*)&mm, (void*)&tm, (void*)&sa};
+        e = cudaLaunchKernel(k1, dim3(p.G1), dim3(stats_threads(p.B)), args, p.smem1, st);
     }
-    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k1_stats launch");
     ++launches;
     InitArgs ia;
     ia.cs = col_state(p, ws, ctx->s_dev);
-    ia.pilot = sa.pilot;
+    ia.pil32 = pa.pil32;
     ia.part1 = sa.part1;
     ia.mean_out = mean_out;
     ia.cov_out = cov_out;
     ia.cols = p.cols;
     ia.N = p.N;
     ia.B = p.B;
-    ia.nch1 = p.nch1;
-    ia.nblk = p.nblk;
+    ia.W1 = p.W1;
+    ia.tpc = p.tpc1;
+    ia.G1 = p.G1;
+    ia.S1 = p.S1;
+    ia.ttot = p.ttot1;
     ia.use_albedo = ctx->use_albedo;
     ia.stats_only = stats_only;
     ia.ridge_rel = ctx->ridge;
@@ -482,7 +567,7 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     }
     unsigned char* ws = (unsigned char*)workspace;
     int launches = 0;
-    smf_status rc = launch_stats(ctx, p, radiance, ws, mm, tm, st, nullptr, nullptr, 0, launches);
+    smf_status rc = launch_stats(ctx, p, radiance, ws, st, nullptr, nullptr, 0, launches);
     if (rc != SMF_OK) return rc;
     ColState cs = col_state(p, ws, ctx->s_dev);
     SweepArgs sa;
@@ -516,14 +601,16 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     ua.G = p.G;
     ua.S = p.S;
     ua.ttot = p.ttot;
+    cudaError_t e0 = cudaFuncSetAttribute(k2_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(p.B * p.B * 8));
+    if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k2_update smem attribute");
     void* kfn = sweep_kernel(p.B);
-    cudaError_t e0 = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem3);
+    e0 = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem3);
     if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k3_sweep smem attribute");
     for (int k = 0; k <= ctx->n_iter; ++k) {
         if (k > 0) {
             {
                 ProfScope ps(ctx, st, SMF_KERNEL_UPDATE);
-                k2_update<<<cols, 128, 0, st>>>(ua);
+                k2_update<<<cols, 128, (size_t)p.B * p.B * 8, st>>>(ua);
             }
             e0 = cudaGetLastError();
             if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k2_update launch");
@@ -648,15 +735,9 @@ smf_status smf_initial_statistics(smf_ctx* ctx, const float* radiance, int cols,
     if (v != SMF_OK) return v;
     Plan p;
     make_plan(ctx, cols, pixels, p);
-    CUtensorMap mm, tm;
-    CUresult cr = make_maps(radiance, cols, pixels, ctx->bands, &mm, &tm);
-    if (cr != CUDA_SUCCESS) {
-        set_err(ctx, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
-        return SMF_ERR_CUDA;
-    }
     int launches = 0;
-    return launch_stats(ctx, p, radiance, (unsigned char*)workspace, mm, tm, (cudaStream_t)stream, mean_out, cov_out,
-                        1, launches);
+    return launch_stats(ctx, p, radiance, (unsigned char*)workspace, (cudaStream_t)stream, mean_out, cov_out, 1,
+                        launches);
 }
 
 }  // extern "C"

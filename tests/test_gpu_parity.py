@@ -78,7 +78,8 @@ def test_tiny_parity(smf, torch, kw):
     rep = assert_parity(enh, alb, a_ref, r_ref, f"tiny {kw}")
     if kw["n_iter"] >= 1:
         assert (enh >= 0).all() and not np.signbit(enh).any()
-    assert nl == 2 + (kw["n_iter"] + 1) + kw["n_iter"] + 1
+    # K0 pilot + K1 stats + K2 init, (N_iter + 1) sweeps, N_iter updates, status copy
+    assert nl == 3 + (kw["n_iter"] + 1) + kw["n_iter"] + 1
     print(rep)
 
 
