@@ -145,8 +145,9 @@ def cpu_baseline(cfg, cube, s, n_iter, sample_cols=None, impl_note="oracle"):
     import oracle
     threads = oracle.max_threads()
     if sample_cols is None:
-        # ~1 s of oracle work per core-column at N = 20000, B = 72 (35 ms / column-iteration)
-        sample_cols = max(1, min(cfg.cols, threads))
+        # ~1 s of oracle work per core-column at N = 20000, B = 72 (35 ms / column-iteration):
+        # 16 columns per thread -> ~15 s of CPU work (bounded sample)
+        sample_cols = max(1, min(cfg.cols, 16 * threads))
     cols = np.linspace(0, cfg.cols - 1, sample_cols).astype(int)
     sub = np.ascontiguousarray(cube[cols])
     t0 = time.perf_counter()
@@ -167,7 +168,8 @@ def run_reference(args, cfg):
     import oracle
     oracle.build()
     threads = oracle.max_threads()
-    sample = args.cpu_sample_cols or max(1, min(cfg.cols, threads))
+    # each reference step: 2 columns per host thread (~2 s), so K + W steps end in minutes
+    sample = args.cpu_sample_cols or max(1, min(cfg.cols, 2 * threads))
     for _ in range(args.warmup):
         cpu_baseline(cfg, cube, s, cfg.n_iter, sample)
     vals = []
