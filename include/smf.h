@@ -148,6 +148,17 @@ smf_status smf_initial_statistics(smf_ctx* ctx, const float* radiance, int cols,
                                   double* mean_out, double* cov_out, void* workspace,
                                   void* stream);
 
+/* Which kernel computes the initial statistics (Fig. alg lines 2-3, the
+ * batched bands x bands SYRK): SMF_STATS_AUTO (default: tensor cores where the
+ * shape fits, FFMA register tiles otherwise), SMF_STATS_FFMA (fp32 FFMA 8x8
+ * register tiles), SMF_STATS_TENSOR (tcgen05 kind::tf32 with the two-term
+ * accuracy-preserving split of DESIGN.md 5.5; SMF_ERR_SHAPE if this band count
+ * has no tensor-core variant). smf_stats_kernel_used returns the kernel AUTO
+ * resolves to (SMF_STATS_FFMA or SMF_STATS_TENSOR), -1 for a NULL context. */
+enum { SMF_STATS_AUTO = 0, SMF_STATS_FFMA = 1, SMF_STATS_TENSOR = 2 };
+smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind);
+int smf_stats_kernel_used(const smf_ctx* ctx);
+
 /* Kernel launches enqueued by the last smf_retrieve call on this context. */
 int smf_last_launch_count(const smf_ctx* ctx);
 

@@ -188,6 +188,9 @@ __device__ __forceinline__ void sts4(uint32_t a, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");
 }
+__device__ __forceinline__ void sts1(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -300,6 +303,7 @@ __global__ void __launch_bounds__(K1Geom<NQ>::NT, 1)
 #pragma unroll
                 for (int q = NQ + 1; q < K::BE / 4; ++q) sts4(xr + q * 16, make_float4(0.f, 0.f, 0.f, 0.f));
             }
+            fence_proxy_async();   // generic reads of stage s before its TMA (async-proxy) refill
             __syncwarp();
             // TMA stage s has been read by every lane: refill it
             if (lane == 0 && i + kStagesK1 < ntl) issue(i + kStagesK1);
@@ -399,6 +403,305 @@ __global__ void __launch_bounds__(K1Geom<NQ>::NT, 1)
     if (cur >= 0) fold(true, cur - cfirst);
 }
 
+// ---------------------------------------------------------------- K1 on tensor cores
+// The same extended-row SYRK as k1_stats (row e = [x_0 .. x_{B-1}, rho, 1, 0 ..],
+// x = L - sigma c), as tcgen05 kind::tf32 MMAs with an
+// accuracy-preserving two-term split: e = h + l with h = tf32_rna(e) and l = e - h
+// (exact in fp32), and
+//     P = h h^T + 2 h l^T,   sym(P) = (P + P^T)/2 = h h^T + h l^T + l h^T,
+// (the MMA computes D = [h h^T | h l^T] and the epilogue folds D1 + 2 D2),
+// i.e. 3xTF32 with the symmetric cross term folded into one operand (the dropped
+// l l^T is ~2^-22 relative). One MMA per 8 pixels: A = H (M = 128 >= BE rows; rows
+// beyond BE are ignored), B = [H | L] (N = 2 BE rows), both K-major (pixels
+// contiguous) SWIZZLE_128B images of a 64-pixel tile (two 32-pixel K-blocks of
+// 128-byte rows) written by the transform warps. (MN-major tf32 operands, which
+// would let the TMA tile feed the MMA directly, produce zeros on this part --
+// measured with scripts/debug/umma_probe.cu.) D (128 x 2 BE fp32) lives in TMEM,
+// double-buffered. Every kFlushTC tiles and at column ends the epilogue warps fold
+// D[:, :BE] + 2 D[:, BE:] into an fp64 shared-memory accumulator (fixed order); at
+// column ends they write it as the column slot's partial P (full BE x BE,
+// row-major) that k2_init symmetrises and reduces in fp64.
+//
+// Warp roles (13 warps): 0-7 transform (group g = warp/4 takes tiles i = g mod 2,
+// two threads per pixel), 8..8+NEPI-1 epilogue (TMEM lanes 32(w%4)..), 11 TMA
+// producer, 12 TMEM allocator + MMA issuer.
+constexpr int kTileTC = 64;       // pixels per tile (8 MMA K-steps of 8)
+#ifndef SMF_K1TC_FLUSH
+#define SMF_K1TC_FLUSH 4
+#endif
+constexpr int kFlushTC = SMF_K1TC_FLUSH;   // tiles per fp32 TMEM accumulation run (256 pixels)
+constexpr int kOpStagesTC = 2;    // operand ring depth (= transform pairs)
+
+template <int NQ>
+struct K1TC {
+    static constexpr int B4 = NQ * 4;
+    static constexpr int BE = (B4 + 2 + 15) / 16 * 16;      // extended row (x16 TMEM loads)
+    static constexpr int NCOL = 2 * BE;                      // MMA N
+    static constexpr int ROWS = NCOL < 128 ? 128 : NCOL;     // operand rows per K-block (A reads 128)
+    static constexpr int REG = ROWS * 128;                   // bytes per 32-pixel K-block
+    static constexpr int OPSTAGE = 2 * REG;
+    using Raw = SweepGeom<NQ, kTileTC>;
+    static constexpr int ACC_LD = BE + 1;                    // odd stride: conflict-free fp64 rows
+    static constexpr size_t ACC_BYTES = ((size_t)BE * ACC_LD * 8 + 1023) / 1024 * 1024;
+    static constexpr size_t BASE = (size_t)kOpStagesTC * OPSTAGE + ACC_BYTES + 1024;
+    static constexpr size_t LIMIT = 227 * 1024 - 4096;       // leave room for static smem
+    // raw ring depth: a multiple of the 2 transform groups, so every stage (and the
+    // parity of its mbarrier phases) is only ever waited on by one group in order --
+    // with an odd depth a group could run two phases ahead and pass a stale parity
+    static constexpr int RS = BASE + 4 * (size_t)Raw::STAGE <= LIMIT ? 4 : 2;
+    static constexpr size_t SMEM = BASE + (size_t)RS * Raw::STAGE;
+    static constexpr int NEPI = (BE + 31) / 32;
+    static constexpr bool FITS = SMEM <= LIMIT && NCOL <= 256 && NEPI <= 3;
+    static constexpr int TMEM_COLS = 2 * NCOL <= 32 ? 32 : 2 * NCOL <= 64 ? 64 : 2 * NCOL <= 128 ? 128
+                                   : 2 * NCOL <= 256 ? 256 : 512;
+    static constexpr int NT = 13 * 32;
+    // transform split: part 0 quads [0, H0), part 1 quads [H0, NQ] (incl. the rho quad); H0 odd
+    static constexpr int H0 = (NQ / 2) % 2 == 1 ? NQ / 2 : NQ / 2 + 1;
+    static constexpr int HQ = (H0 > NQ + 1 - H0) ? H0 : NQ + 1 - H0;   // max quads per part
+    // instruction descriptor: D f32, A/B tf32, both K-major, N = NCOL, M = 128
+    static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NCOL >> 3) << 17) |
+                                      ((uint32_t)(128 >> 4) << 24);
+};
+
+template <int NQ>
+__global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
+    k1_stats_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__ CUtensorMap tm_tail,
+                StatsArgs a) {
+    using K = K1TC<NQ>;
+    using Raw = typename K::Raw;
+    constexpr int B4 = K::B4;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* ops = align1024(smem_raw);                                    // [OS][OPSTAGE]
+    unsigned char* raws = ops + kOpStagesTC * K::OPSTAGE;                       // [RS][Raw::STAGE]
+    double* acc = reinterpret_cast<double*>(raws + K::RS * Raw::STAGE);         // [BE][BE+1]
+    __shared__ uint64_t raw_full[K::RS], raw_empty[K::RS], op_full[kOpStagesTC], op_empty[kOpStagesTC];
+    __shared__ uint64_t acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_sh;
+    __shared__ __align__(16) float pil[8][B4];
+    __shared__ __align__(16) float gh[8][B4];
+
+    const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    const long long tb = tile_begin(blockIdx.x, a.ttot, a.G), te = tile_begin(blockIdx.x + 1, a.ttot, a.G);
+    const int ntl = (int)(te - tb);
+    const int cfirst = (int)(tb / a.tpc);
+
+    // zero the operand ring (padding entries and unused chunks stay zero) and the accumulator
+    for (int i = tid; i < kOpStagesTC * K::OPSTAGE / 16; i += K::NT)
+        reinterpret_cast<float4*>(ops)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = tid; i < K::BE * K::ACC_LD; i += K::NT) acc[i] = 0.0;
+    if (tid == 0) {
+        for (int s = 0; s < K::RS; ++s) {
+            mbar_init(&raw_full[s], 1);
+            mbar_init(&raw_empty[s], 4);
+        }
+        for (int o = 0; o < kOpStagesTC; ++o) {
+            mbar_init(&op_full[o], 4);
+            mbar_init(&op_empty[o], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], K::NEPI);
+        }
+        fence_mbar_init();
+    }
+    if (wid == 12) tmem_alloc(&tmem_sh, K::TMEM_COLS);
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_sh;
+
+    if (wid < 8) {
+        // ===================== transform: raw tile -> [H | L] operand image =====================
+        // group g = wid / 4 takes tiles i = g mod 2 (operand stage g); warp w4 = wid % 4 takes
+        // pixels 16 w4 .. 16 w4 + 15; lane = (part << 4) | pixel: part 0 handles quads
+        // [0, H0), part 1 quads [H0, NQ) and the (rho, 1) quad. H0 is odd, so the two parts'
+        // rows b and b + 4 H0 hit complementary swizzle chunks: conflict-free 4-byte stores.
+        constexpr int H0 = K::H0;
+        const int grp = wid >> 2, w4 = wid & 3, part = lane >> 4;
+        const int row = 16 * w4 + (lane & 15);                // pixel within the tile
+        const int q0 = part ? H0 : 0;
+        const int nqp = part ? NQ + 1 - H0 : H0;              // quads of this part (part 1: incl. rho quad)
+        const uint32_t raw0 = smem_u32(raws), ops0 = smem_u32(ops);
+        uint32_t qo[K::HQ];
+#pragma unroll
+        for (int q = 0; q < K::HQ; ++q) qo[q] = Raw::quad_off(row, q0 + q < NQ ? q0 + q : NQ - 1);
+        // K-major SWIZZLE_128B image: entry b of this pixel at row b of K-block row/32,
+        // 16-byte chunk ((row%32)/4) ^ (b & 7), word row & 3
+        const uint32_t kch = (uint32_t)((row & 31) >> 2);
+        uint32_t abase[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+            abase[jj] = (uint32_t)(row >> 5) * K::REG + (uint32_t)(row & 3) * 4 + (uint32_t)q0 * 4 * 128 +
+                        ((kch ^ (uint32_t)jj ^ (uint32_t)((4 * q0) & 7)) << 4);
+        TileCursor cur(tb + grp, a.tpc);
+        int ccol = -1;
+        for (int i = grp; i < ntl; i += 2) {
+            const int c = cur.c, row0 = cur.tt * kTileTC;
+            cur.next();
+            cur.next();
+            if (c != ccol) {
+                __syncwarp();
+                for (int b = lane; b < B4; b += 32) {
+                    pil[wid][b] = a.pil32[(size_t)c * a.B + b];
+                    gh[wid][b] = a.ghat32[(size_t)c * a.B + b];
+                }
+                __syncwarp();
+                ccol = c;
+            }
+            const int s = i % K::RS, o = i % kOpStagesTC;
+            const bool valid = row0 + row < a.N;   // rows beyond N arrive zero-filled by TMA
+            mbar_wait(&raw_full[s], (i / K::RS) & 1);
+            float4 v[K::HQ];
+            float sgp[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int q = 0; q < K::HQ; ++q) {
+                if (q < nqp && q0 + q < NQ) {
+                    v[q] = lds4(raw0 + s * Raw::STAGE + qo[q]);
+                    sgp[q & 3] = dot4(v[q], *reinterpret_cast<const float4*>(&gh[wid][4 * (q0 + q)]), sgp[q & 3]);
+                }
+            }
+            float sg = (sgp[0] + sgp[1]) + (sgp[2] + sgp[3]);
+            sg += __shfl_xor_sync(0xffffffffu, sg, 16);
+            // order this thread's generic-proxy reads of the raw stage before the TMA
+            // (async proxy) refill that the release below allows -- without it the
+            // refill was measured to overwrite rows still being read
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&raw_empty[s]);   // every lane has consumed its raw row
+            if (i >= kOpStagesTC) mbar_wait(&op_empty[o], ((i / kOpStagesTC) - 1) & 1);
+            const uint32_t ob = ops0 + o * K::OPSTAGE;
+#pragma unroll
+            for (int q = 0; q < K::HQ; ++q) {
+                const int qq = q0 + q;   // global quad of this thread's q-th quad
+                if (q >= nqp) break;
+                float xs[4];
+                if (qq < NQ) {
+                    const float4 cq = *reinterpret_cast<const float4*>(&pil[wid][4 * qq]);
+                    xs[0] = fmaf(-sg, cq.x, v[q].x);
+                    xs[1] = fmaf(-sg, cq.y, v[q].y);
+                    xs[2] = fmaf(-sg, cq.z, v[q].z);
+                    xs[3] = fmaf(-sg, cq.w, v[q].w);
+                } else {
+                    xs[0] = valid ? sg - 1.f : 0.f;
+                    xs[1] = valid ? 1.f : 0.f;
+                }
+#pragma unroll
+                for (int j2 = 0; j2 < 4; ++j2) {
+                    if (qq == NQ && j2 >= 2) break;   // padding rows stay zero
+                    const int jb = 4 * q + j2;       // entry relative to this part's first band
+                    const float x = xs[j2];
+                    const float h = tf32_rna(x);
+                    const float l = x - h;   // exact; the MMA reads it as tf32 (low-part rounding
+                                             // measured to make no difference)
+                    const uint32_t ad = ob + abase[jb & 7] + (uint32_t)jb * 128;
+                    sts1(ad, h);
+                    sts1(ad + (uint32_t)K::BE * 128, l);
+                }
+            }
+            fence_proxy_async();   // generic-proxy smem writes -> visible to the tensor core
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&op_full[o]);
+        }
+    } else if (wid >= 8 && wid < 8 + K::NEPI) {
+        // ===================== epilogue: TMEM -> fp64 shared accumulator -> partials =====================
+        const int e = wid - 8, m = 32 * e + lane;
+        const bool live = m < K::BE;
+        double* arow = acc + (size_t)(live ? m : 0) * K::ACC_LD;
+        TileCursor cur(tb, a.tpc);
+        int g = 0, run = 0;
+        for (int i = 0; i < ntl; ++i) {
+            const int c = cur.c;
+            cur.next();
+            const bool col_end = (i == ntl - 1) || cur.c != c;
+            ++run;
+            if (!col_end && run < kFlushTC) continue;
+            run = 0;
+            const int ab = g & 1;
+            mbar_wait(&acc_full[ab], (g >> 1) & 1);
+            tc_fence_after();
+            const uint32_t t0 = tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)(ab * K::NCOL);
+#pragma unroll 1
+            for (int n0 = 0; n0 < K::BE; n0 += 16) {
+                float v[16], u[16];
+                tmem_ld16x2(t0 + n0, t0 + K::BE + n0, v, u);
+                if (live) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) arow[n0 + j] += (double)v[j] + 2.0 * (double)u[j];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            ++g;
+            if (col_end && live) {
+                double* out = a.part1 + (((size_t)blockIdx.x * a.S + (c - cfirst)) * K::BE + m) * K::BE;
+                for (int n = 0; n < K::BE; ++n) {
+                    out[n] = arow[n];
+                    arow[n] = 0.0;
+                }
+            }
+        }
+    } else if (wid == 11) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            prefetch_tmap(&tm_main);
+            if (Raw::TAILW) prefetch_tmap(&tm_tail);
+            TileCursor cur(tb, a.tpc);
+            for (int i = 0; i < ntl; ++i) {
+                const int s = i % K::RS;
+                if (i >= K::RS) mbar_wait(&raw_empty[s], ((i / K::RS) - 1) & 1);
+                const int c = cur.c, row0 = cur.tt * kTileTC;
+                cur.next();
+                unsigned char* st = raws + s * Raw::STAGE;
+                mbar_arrive_expect_tx(&raw_full[s], Raw::TX);
+#pragma unroll
+                for (int f = 0; f < Raw::NFULL; ++f)
+                    tma_load_3d(st + f * (kTileTC * 128), &tm_main, &raw_full[s], f * 32, row0, c);
+                if (Raw::TAILW)
+                    tma_load_3d(st + Raw::NFULL * (kTileTC * 128), &tm_tail, &raw_full[s], Raw::NFULL * 32, row0, c);
+            }
+        }
+    } else if (wid == 12) {
+        // ===================== MMA issuer (one thread) =====================
+        if (lane == 0) {
+            const uint32_t ops0 = smem_u32(ops);
+            TileCursor cur(tb, a.tpc);
+            int g = 0, run = 0;
+            bool fresh = true;
+            for (int i = 0; i < ntl; ++i) {
+                const int c = cur.c;
+                cur.next();
+                const bool col_end = (i == ntl - 1) || cur.c != c;
+                const int o = i % kOpStagesTC, ab = g & 1;
+                if (fresh && g >= 2) mbar_wait(&acc_empty[ab], ((g >> 1) - 1) & 1);
+                mbar_wait(&op_full[o], (i / kOpStagesTC) & 1);
+                tc_fence_after();
+                const uint32_t sa = ops0 + o * K::OPSTAGE;
+#pragma unroll
+                for (int ks = 0; ks < kTileTC / 8; ++ks) {
+                    const uint64_t d = umma_desc(sa + (ks >> 2) * K::REG + (ks & 3) * 32, 16, 1024, 2);
+                    mma_tf32(tmem + (uint32_t)(ab * K::NCOL), d, d, K::IDESC, (fresh && ks == 0) ? 0u : 1u);
+                }
+                fresh = false;
+                mma_commit(&op_empty[o]);
+                if (col_end || ++run == kFlushTC) {
+                    mma_commit(&acc_full[ab]);
+                    ++g;
+                    run = 0;
+                    fresh = true;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (wid == 12) {
+        tc_fence_after();
+        tmem_dealloc(tmem, K::TMEM_COLS);
+    }
+}
+
 // Pilot per column: c = fp32 mean of the first kPilotRows pixels, ghat = c/|c|^2.
 struct PilotArgs {
     const float* L;
@@ -480,6 +783,7 @@ struct InitArgs {
     double* mean_out;      // optional [cols][B] (smf_initial_statistics)
     double* cov_out;       // optional [cols][B][B]
     int cols, N, B, W1, tpc, G1, S1, use_albedo, stats_only;
+    int be_full;           // > 0: K1 partials are full BE x BE row-major P (k1_stats_tc), symmetrised here
     long long ttot;
     double ridge_rel;
 };
@@ -489,12 +793,14 @@ __host__ inline int k1_width_host(int B) {
     return nblk * (nblk + 1) / 2 * 64;
 }
 
-__host__ inline size_t k2_init_smem(int B) {
-    return (size_t)B * B * 8 + (size_t)k1_width_host(B) * 8 + 6 * (size_t)B * 8 + 32 * 4 * 8;
+__host__ inline size_t k2_init_smem(int B, int W1) {
+    return (size_t)B * B * 8 + (size_t)W1 * 8 + 6 * (size_t)B * 8 + 32 * 4 * 8;
 }
 
-// entry (i, k), i >= k, of the extended-row block sums
-__device__ __forceinline__ double ext_entry(const double* S, int i, int k) {
+// entry (i, k) of the extended-row second-moment sums: be > 0 -> symmetrised full
+// BE x BE matrix (tensor-core K1: (P + P^T)/2), else the 8x8-blocked lower triangle
+__device__ __forceinline__ double ext_entry(const double* S, int i, int k, int be) {
+    if (be > 0) return 0.5 * (S[i * be + k] + S[k * be + i]);
     if (i < k) {
         int t = i;
         i = k;
@@ -536,12 +842,13 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     }
     if (tid == 0) bad = COL_OK;
     __syncthreads();
-    const double Sr = ext_entry(S, B + 1, B), Srr = ext_entry(S, B, B);
+    const int be = a.be_full;
+    const double Sr = ext_entry(S, B + 1, B, be), Srr = ext_entry(S, B, B, be);
     // sum (L - c) = sum x + (sum rho) c ;  dm = mean(L) - c
     for (int b = tid; b < B; b += blockDim.x) {
         cv[b] = (double)a.pil32[(size_t)c * B + b];
-        srx[b] = ext_entry(S, B, b);
-        dm[b] = (ext_entry(S, B + 1, b) + Sr * cv[b]) * invN;
+        srx[b] = ext_entry(S, B, b, be);
+        dm[b] = (ext_entry(S, B + 1, b, be) + Sr * cv[b]) * invN;
     }
     __syncthreads();
     // sum (L-c)(L-c)^T = Sxx + Srx c^T + c Srx^T + Srr c c^T ;  C0 = that/N - dm dm^T
@@ -558,7 +865,7 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
         }
         if (ci < ck) continue;
         const int ii = ci, kk = ck;
-        double s2 = ext_entry(S, ii, kk) + srx[ii] * cv[kk] + cv[ii] * srx[kk] + Srr * cv[ii] * cv[kk];
+        double s2 = ext_entry(S, ii, kk, be) + srx[ii] * cv[kk] + cv[ii] * srx[kk] + Srr * cv[ii] * cv[kk];
         double v = s2 * invN - dm[ii] * dm[kk];
         if (!isfinite(v)) nonfinite = 1;
         A[ii * B + kk] = v;
@@ -1045,6 +1352,7 @@ __global__ void __launch_bounds__(kTileRows, 2)
                 }
             }
         }
+        fence_proxy_async();   // generic reads of stage s before its TMA (async-proxy) refill
         __syncthreads();
         if (tid == 0 && i + kStages < ntl) issue(i + kStages);
     }

@@ -29,6 +29,7 @@ struct smf_ctx {
     bool s_set = false;
     double eps = 1e-2, ridge = 0.0, r_floor = 0.05;
     int n_iter = 30, use_sparsity = 1, use_albedo = 1;
+    int stats_kernel = SMF_STATS_AUTO;
     int last_launches = 0;
     char err[512] = {0};
     // profiling (smf_profile_*): events bracketing each launch
@@ -108,7 +109,8 @@ struct Plan {
     int cols, N, B, tpc, G, S;
     long long ttot;
     // K1 (persistent, one CTA per SM, own tile height T1 and partition)
-    int G1, S1, W1, T1, tpc1;
+    int G1, S1, W1, T1, tpc1, NT1, be_full;
+    bool k1tc;
     long long ttot1;
     size_t smem1, smem2, smem3;
     // workspace offsets
@@ -119,6 +121,10 @@ struct Plan {
 int sweep_blocks_per_sm(int B);
 size_t k1_smem(int B);
 int k1_rows(int B);
+int stats_threads(int B);
+bool k1tc_fits(int B);
+int k1tc_be(int B);
+size_t k1tc_smem(int B);
 
 bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     const int B = ctx->bands;
@@ -137,7 +143,10 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
         if (t1 > t0) S = std::max(S, (int)((t1 - 1) / p.tpc - t0 / p.tpc + 1));
     }
     p.S = S;
-    p.T1 = k1_rows(B);
+    p.k1tc = ctx->stats_kernel != SMF_STATS_FFMA && k1tc_fits(B);
+    p.T1 = p.k1tc ? kTileTC : k1_rows(B);
+    p.NT1 = p.k1tc ? K1TC<1>::NT : stats_threads(B);
+    p.be_full = p.k1tc ? k1tc_be(B) : 0;
     p.tpc1 = (N + p.T1 - 1) / p.T1;
     p.ttot1 = (long long)cols * p.tpc1;
     p.G1 = (int)std::min<long long>(ctx->sm_count, p.ttot1);
@@ -146,10 +155,10 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
         long long t0 = tile_begin(b, p.ttot1, p.G1), t1 = tile_begin(b + 1, p.ttot1, p.G1);
         if (t1 > t0) p.S1 = std::max(p.S1, (int)((t1 - 1) / p.tpc1 - t0 / p.tpc1 + 1));
     }
-    p.W1 = k1_width_host(B);
+    p.W1 = p.k1tc ? p.be_full * p.be_full : k1_width_host(B);
     TileGeom g = TileGeom::make(B);
-    p.smem1 = k1_smem(B);
-    p.smem2 = k2_init_smem(B);
+    p.smem1 = p.k1tc ? k1tc_smem(B) : k1_smem(B);
+    p.smem2 = k2_init_smem(B, p.W1);
     p.smem3 = (size_t)kStages * g.stage_bytes + 1024;
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -233,6 +242,43 @@ void* stats_kernel(int B) {
         SMF_NQ_CASES(SMF_CASE)
 #undef SMF_CASE
         default: return nullptr;
+    }
+}
+
+template <int NQ>
+void* stats_tc_fn() {
+    return reinterpret_cast<void*>(&k1_stats_tc<NQ>);
+}
+
+void* stats_tc_kernel(int B) {
+    switch (B / 4) {
+#define SMF_CASE(n) \
+    case n: return K1TC<n>::FITS ? stats_tc_fn<n>() : nullptr;
+        SMF_NQ_CASES(SMF_CASE)
+#undef SMF_CASE
+        default: return nullptr;
+    }
+}
+
+bool k1tc_fits(int B) { return stats_tc_kernel(B) != nullptr; }
+
+int k1tc_be(int B) {
+    switch (B / 4) {
+#define SMF_CASE(n) \
+    case n: return K1TC<n>::BE;
+        SMF_NQ_CASES(SMF_CASE)
+#undef SMF_CASE
+        default: return 0;
+    }
+}
+
+size_t k1tc_smem(int B) {
+    switch (B / 4) {
+#define SMF_CASE(n) \
+    case n: return K1TC<n>::SMEM;
+        SMF_NQ_CASES(SMF_CASE)
+#undef SMF_CASE
+        default: return 0;
     }
 }
 
@@ -379,13 +425,13 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     sa.G = p.G1;
     sa.S = p.S1;
     sa.ttot = p.ttot1;
-    void* k1 = stats_kernel(p.B);
+    void* k1 = p.k1tc ? stats_tc_kernel(p.B) : stats_kernel(p.B);
     e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k1_stats smem attribute");
     {
         ProfScope ps(ctx, st, SMF_KERNEL_STATS);
         void* args[] = {(void*)&mm, (void*)&tm, (void*)&sa};
-        e = cudaLaunchKernel(k1, dim3(p.G1), dim3(stats_threads(p.B)), args, p.smem1, st);
+        e = cudaLaunchKernel(k1, dim3(p.G1), dim3(p.NT1), args, p.smem1, st);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k1_stats launch");
     ++launches;
@@ -403,6 +449,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     ia.G1 = p.G1;
     ia.S1 = p.S1;
     ia.ttot = p.ttot1;
+    ia.be_full = p.be_full;
     ia.use_albedo = ctx->use_albedo;
     ia.stats_only = stats_only;
     ia.ridge_rel = ctx->ridge;
@@ -536,6 +583,21 @@ smf_status smf_set_iterations(smf_ctx* ctx, int n_iter, int use_sparsity, int us
     ctx->use_sparsity = use_sparsity ? 1 : 0;
     ctx->use_albedo = use_albedo ? 1 : 0;
     return SMF_OK;
+}
+
+smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind) {
+    if (!ctx || kind < SMF_STATS_AUTO || kind > SMF_STATS_TENSOR) return SMF_ERR_INVALID_ARGUMENT;
+    if (kind == SMF_STATS_TENSOR && !k1tc_fits(ctx->bands)) {
+        set_err(ctx, "tensor-core statistics kernel unavailable for %d bands", ctx->bands);
+        return SMF_ERR_SHAPE;
+    }
+    ctx->stats_kernel = kind;
+    return SMF_OK;
+}
+
+int smf_stats_kernel_used(const smf_ctx* ctx) {
+    if (!ctx) return -1;
+    return (ctx->stats_kernel != SMF_STATS_FFMA && k1tc_fits(ctx->bands)) ? SMF_STATS_TENSOR : SMF_STATS_FFMA;
 }
 
 smf_status smf_workspace_bytes(const smf_ctx* ctx, int cols, int pixels, size_t* bytes) {

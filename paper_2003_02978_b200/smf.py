@@ -39,6 +39,8 @@ SYMBOLS = {
     "smf_column_model": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp]),
     "smf_initial_statistics": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp]),
     "smf_last_launch_count": (_i, [_vp]),
+    "smf_set_stats_kernel": (_i, [_vp, _i]),
+    "smf_stats_kernel_used": (_i, [_vp]),
     "smf_profile_enable": (_i, [_vp, _i]),
     "smf_profile_read": (_i, [_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_i)]),
     "smf_status_string": (ctypes.c_char_p, [_i]),
@@ -76,8 +78,10 @@ def _ptr(t):
 class Retriever:
     """A library context (smf_ctx) bound to the current CUDA device."""
 
+    STATS_KERNELS = {"auto": 0, "ffma": 1, "tensor": 2}
+
     def __init__(self, bands, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2, ridge_rel=0.0,
-                 r_floor=0.05):
+                 r_floor=0.05, stats_kernel="auto"):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("smf needs a CUDA device (no CPU fallback)")
@@ -89,7 +93,13 @@ class Retriever:
         self._check(_lib.smf_set_absorption(self._h, s.ctypes.data_as(_vp), self.bands))
         self._check(_lib.smf_set_regularisation(self._h, float(eps), float(ridge_rel), float(r_floor)))
         self._check(_lib.smf_set_iterations(self._h, int(n_iter), int(bool(use_sparsity)), int(bool(use_albedo))))
+        self._check(_lib.smf_set_stats_kernel(self._h, self.STATS_KERNELS[stats_kernel]))
         self.n_iter = int(n_iter)
+
+    @property
+    def stats_kernel_used(self) -> str:
+        """'tensor' (tcgen05 kind::tf32, split) or 'ffma': the kernel computing mu0, C0."""
+        return {1: "ffma", 2: "tensor"}[_lib.smf_stats_kernel_used(self._h)]
 
     def _check(self, rc, h="self"):
         if rc != SMF_OK:

@@ -45,11 +45,14 @@ def oracle_kw(kw):
 
 
 # ------------------------------------------------------------------ K1 statistics
-@pytest.mark.parametrize("name,cols", [("tiny", 8), ("segment", 6)])
-def test_initial_statistics_vs_oracle(smf, torch, name, cols):
+@pytest.mark.parametrize("kernel", ["tensor", "ffma"])
+@pytest.mark.parametrize("name,cols", [("tiny", 8), ("segment", 6), ("flightline", 3)])
+def test_initial_statistics_vs_oracle(smf, torch, name, cols, kernel):
+    """K1 (both statistics kernels) + K2 reduction vs the oracle's mu0 and C0 (Fig. alg lines 2-3)."""
     cfg = synth.scaled(synth.CONFIGS[name], cols=cols)
-    cube, s, _ = synth.generate(cfg)
-    r = smf.Retriever(cfg.bands, s)
+    cube, s, _ = synth.generate(cfg, columns=list(range(cols)))
+    r = smf.Retriever(cfg.bands, s, stats_kernel=kernel)
+    assert r.stats_kernel_used == kernel
     mean, cov = r.initial_statistics(torch.from_numpy(cube).cuda())
     mean, cov = mean.cpu().numpy(), cov.cpu().numpy()
     for c in range(cols):
@@ -68,12 +71,16 @@ VARIANTS = [dict(use_sparsity=1, use_albedo=1, n_iter=10), dict(use_sparsity=1, 
             dict(use_sparsity=1, use_albedo=1, n_iter=30)]
 
 
-@pytest.mark.parametrize("kw", VARIANTS, ids=lambda k: f"sp{k['use_sparsity']}al{k['use_albedo']}it{k['n_iter']}")
+VARIANTS += [dict(use_sparsity=1, use_albedo=1, n_iter=10, stats_kernel="ffma")]
+
+
+@pytest.mark.parametrize("kw", VARIANTS, ids=lambda k: f"sp{k['use_sparsity']}al{k['use_albedo']}it{k['n_iter']}"
+                         + k.get("stats_kernel", ""))
 def test_tiny_parity(smf, torch, kw):
     cfg = synth.CONFIGS["tiny"]
     cube, s, _ = synth.generate(cfg)
     enh, alb, st, mu, q, nl = run_gpu(smf, torch, cube, s, **kw)
-    a_ref, r_ref, st_ref = oracle.retrieve(cube, s, **oracle_kw(kw))
+    a_ref, r_ref, st_ref = oracle.retrieve(cube, s, **oracle_kw({k: v for k, v in kw.items() if k != "stats_kernel"}))
     assert (st == 0).all() and (st_ref == 0).all()
     rep = assert_parity(enh, alb, a_ref, r_ref, f"tiny {kw}")
     if kw["n_iter"] >= 1:
@@ -103,9 +110,12 @@ def test_segment_columns_parity(smf, torch):
     rep = assert_parity(enh, alb, a_ref, r_ref, "segment")
     print(rep)
     assert rep["zero_set_agreement"] > 0.999
+    # q^{N_iter} is reported (C18), not part of the north_star bar; 1e-4 bounds the
+    # tensor-core statistics kernel (C0 rel. error ~5e-7, amplified ~60x by 30 iterations
+    # at cond(C) ~1e5) as in the flightline test
     for j in range(2):
         q_ref = oracle.retrieve_column(cube[j], s, n_iter=cfg.n_iter, diagnostics=True)[3]["q"][-1]
-        assert abs(q[j] / q_ref - 1) < 1e-5
+        assert abs(q[j] / q_ref - 1) < 1e-4
 
 
 @pytest.mark.parametrize("j,n_iter,sp", [(3, 30, 1), (1, 30, 1), (0, 0, 0)])
