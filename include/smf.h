@@ -125,10 +125,14 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
 smf_status smf_synchronize(smf_ctx* ctx, void* stream, const int32_t* column_status, int cols,
                            int* first_failed_column);
 
-/* End-to-end convenience call with HOST buffers (pinned or pageable):
- * copies radiance host->device, runs smf_retrieve on an internal stream with
- * context-owned device buffers (grown on demand and reused across calls),
- * copies enhancement, albedo and column_status device->host and synchronises.
+/* End-to-end convenience call with HOST buffers (pinned for full overlap;
+ * pageable works): streams the cube through the device in column chunks (columns
+ * are independent partitions) -- the host->device copy of chunk i+1
+ * overlaps smf_retrieve of chunk i and the device->host copy of chunk i-1 on three
+ * internal streams, with context-owned device buffers (two chunk slots + one
+ * workspace, grown on demand and reused across calls) -- then synchronises.
+ * Each chunk's results are bitwise those of smf_retrieve on the same columns (the
+ * whole-cube launch differs only in the per-column fp reduction order).
  * Returns SMF_ERR_NUMERICAL if any column failed. */
 smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols, int pixels,
                              float* enhancement_host, float* albedo_host,

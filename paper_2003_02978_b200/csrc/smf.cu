@@ -38,7 +38,10 @@ struct smf_ctx {
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
     // smf_retrieve_host state
-    cudaStream_t h_stream = nullptr;
+    cudaStream_t h_stream = nullptr;   // compute
+    cudaStream_t h_up = nullptr;       // host -> device copies
+    cudaStream_t h_down = nullptr;     // device -> host copies
+    cudaEvent_t h_ev[8] = {};          // [0,2) uploaded, [2,4) computed, [4,6) downloaded
     void* h_buf = nullptr;
     size_t h_buf_bytes = 0;
 };
@@ -546,6 +549,10 @@ void smf_destroy(smf_ctx* ctx) {
     cudaFree(ctx->s_dev);
     if (ctx->h_buf) cudaFree(ctx->h_buf);
     if (ctx->h_stream) cudaStreamDestroy(ctx->h_stream);
+    if (ctx->h_up) cudaStreamDestroy(ctx->h_up);
+    if (ctx->h_down) cudaStreamDestroy(ctx->h_down);
+    for (auto ev : ctx->h_ev)
+        if (ev) cudaEventDestroy(ev);
     delete ctx;
 }
 
@@ -726,19 +733,31 @@ smf_status smf_synchronize(smf_ctx* ctx, void* stream, const int32_t* column_sta
 
 smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols, int pixels,
                              float* enhancement_host, float* albedo_host, int32_t* column_status_host) {
+    // Columns are independent partitions, so the cube is streamed in column
+    // chunks through two device buffers: the upload of chunk i+1 (copy engine, h_up)
+    // overlaps the retrieval of chunk i (h_stream) and the download of chunk i-1 (h_down).
     if (!ctx || !radiance_host || !enhancement_host || !albedo_host || cols < 1 || pixels < 2)
         return SMF_ERR_INVALID_ARGUMENT;
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
     if (!ctx->h_stream) {
         e = cudaStreamCreateWithFlags(&ctx->h_stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->h_up, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->h_down, cudaStreamNonBlocking);
+        for (int k = 0; k < 6 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&ctx->h_ev[k], cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "stream create");
     }
-    size_t ws_bytes = 0;
-    smf_workspace_bytes(ctx, cols, pixels, &ws_bytes);
-    const size_t rad_bytes = align_up((size_t)cols * pixels * ctx->bands * 4, 256);
-    const size_t map_bytes = align_up((size_t)cols * pixels * 4, 256);
+    const int nchunks = std::max(1, std::min(8, cols / 64));
+    const int ccols = (cols + nchunks - 1) / nchunks;   // columns per chunk (last may be short)
+    size_t ws_bytes = 0, ws_last = 0;
+    smf_workspace_bytes(ctx, ccols, pixels, &ws_bytes);
+    smf_workspace_bytes(ctx, cols - (nchunks - 1) * ccols > 0 ? cols - (nchunks - 1) * ccols : ccols, pixels,
+                        &ws_last);
+    ws_bytes = std::max(ws_bytes, ws_last);
+    const size_t col_rad = (size_t)pixels * ctx->bands * 4, col_map = (size_t)pixels * 4;
+    const size_t rad_bytes = align_up((size_t)ccols * col_rad, 256);
+    const size_t map_bytes = align_up((size_t)ccols * col_map, 256);
     const size_t st_bytes = align_up((size_t)cols * 4, 256);
-    const size_t need = rad_bytes + 2 * map_bytes + st_bytes + ws_bytes;
+    const size_t need = 2 * (rad_bytes + 2 * map_bytes) + st_bytes + ws_bytes;
     if (need > ctx->h_buf_bytes) {
         if (ctx->h_buf) cudaFree(ctx->h_buf);
         ctx->h_buf = nullptr;
@@ -748,23 +767,56 @@ smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols,
         ctx->h_buf_bytes = need;
     }
     unsigned char* b = (unsigned char*)ctx->h_buf;
-    float* d_rad = (float*)b;
-    float* d_enh = (float*)(b + rad_bytes);
-    float* d_alb = (float*)(b + rad_bytes + map_bytes);
-    int32_t* d_st = (int32_t*)(b + rad_bytes + 2 * map_bytes);
-    void* d_ws = b + rad_bytes + 2 * map_bytes + st_bytes;
-    cudaStream_t st = ctx->h_stream;
-    e = cudaMemcpyAsync(d_rad, radiance_host, (size_t)cols * pixels * ctx->bands * 4, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D radiance");
-    smf_status rc = smf_retrieve(ctx, d_rad, cols, pixels, d_enh, d_alb, d_ws, d_st, st);
-    if (rc != SMF_OK) return rc;
-    e = cudaMemcpyAsync(enhancement_host, d_enh, (size_t)cols * pixels * 4, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(albedo_host, d_alb, (size_t)cols * pixels * 4, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess && column_status_host)
-        e = cudaMemcpyAsync(column_status_host, d_st, (size_t)cols * 4, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "retrieve_host D2H");
+    float *d_rad[2], *d_enh[2], *d_alb[2];
+    for (int k = 0; k < 2; ++k) {
+        unsigned char* base = b + k * (rad_bytes + 2 * map_bytes);
+        d_rad[k] = (float*)base;
+        d_enh[k] = (float*)(base + rad_bytes);
+        d_alb[k] = (float*)(base + rad_bytes + map_bytes);
+    }
+    int32_t* d_st = (int32_t*)(b + 2 * (rad_bytes + 2 * map_bytes));
+    void* d_ws = b + 2 * (rad_bytes + 2 * map_bytes) + st_bytes;
+    cudaEvent_t* up = ctx->h_ev;          // chunk i uploaded into slot i % 2
+    cudaEvent_t* done = ctx->h_ev + 2;    // chunk i computed
+    cudaEvent_t* down = ctx->h_ev + 4;    // chunk i downloaded (slot free)
+    int launches = 0;
+    for (int i = 0; i < nchunks; ++i) {
+        const int c0 = i * ccols, nc = std::min(ccols, cols - c0), k = i & 1;
+        if (nc <= 0) break;
+        // upload: slot k is free once chunk i-2 has been computed
+        if (i >= 2) e = cudaStreamWaitEvent(ctx->h_up, done[k], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d_rad[k], radiance_host + (size_t)c0 * pixels * ctx->bands, (size_t)nc * col_rad,
+                                cudaMemcpyHostToDevice, ctx->h_up);
+        if (e == cudaSuccess) e = cudaEventRecord(up[k], ctx->h_up);
+        // compute: after the upload, and after chunk i-2's outputs have left slot k
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->h_stream, up[k], 0);
+        if (e == cudaSuccess && i >= 2) e = cudaStreamWaitEvent(ctx->h_stream, down[k], 0);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "retrieve_host upload");
+        smf_status rc = smf_retrieve(ctx, d_rad[k], nc, pixels, d_enh[k], d_alb[k], d_ws, d_st + c0, ctx->h_stream);
+        if (rc != SMF_OK) return rc;
+        launches += ctx->last_launches;
+        e = cudaEventRecord(done[k], ctx->h_stream);
+        // download
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->h_down, done[k], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(enhancement_host + (size_t)c0 * pixels, d_enh[k], (size_t)nc * col_map,
+                                cudaMemcpyDeviceToHost, ctx->h_down);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(albedo_host + (size_t)c0 * pixels, d_alb[k], (size_t)nc * col_map,
+                                cudaMemcpyDeviceToHost, ctx->h_down);
+        if (e == cudaSuccess) e = cudaEventRecord(down[k], ctx->h_down);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "retrieve_host download");
+    }
+    ctx->last_launches = launches;
+    if (column_status_host) {
+        e = cudaStreamWaitEvent(ctx->h_down, done[(nchunks - 1) & 1], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(column_status_host, d_st, (size_t)cols * 4, cudaMemcpyDeviceToHost, ctx->h_down);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->h_down);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->h_stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "retrieve_host sync");
     if (column_status_host)
         for (int c = 0; c < cols; ++c)
             if (column_status_host[c] != SMF_COL_OK) return SMF_ERR_NUMERICAL;

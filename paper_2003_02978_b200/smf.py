@@ -107,9 +107,10 @@ class Retriever:
             raise SMFError(rc, msg)
 
     def close(self):
-        if getattr(self, "_h", None):
-            _lib.smf_destroy(self._h)
-            self._h = None
+        lib = globals().get("_lib")   # None during interpreter shutdown
+        if getattr(self, "_h", None) and lib is not None:
+            lib.smf_destroy(self._h)
+        self._h = None
 
     __del__ = close
 

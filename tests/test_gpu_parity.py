@@ -215,6 +215,25 @@ def test_determinism_and_host_path(smf, torch):
     np.testing.assert_array_equal(ah, a1)
 
 
+def test_host_path_chunked(smf, torch):
+    """smf_retrieve_host streams column chunks (3 here) through two device slots with
+    overlapped copies. Each chunk equals a device-resident retrieval of the same columns
+    bit for bit; against the whole-cube launch only the per-column reduction order (the
+    CTA partition) differs, so that comparison uses the C18 bar."""
+    cfg = synth.scaled(synth.CONFIGS["segment"], cols=200, pixels=1000)
+    cube, s, _ = synth.generate(cfg)
+    r = smf.Retriever(cfg.bands, s, n_iter=30)
+    eh, ah, sh, rc = r.retrieve_host(cube)
+    assert rc == 0 and (sh == 0).all()
+    chunk = 67   # 200 columns -> 3 chunks of ceil(200/3)
+    for c0 in range(0, 200, chunk):
+        ec, ac, stc, *_ = run_gpu(smf, torch, cube[c0:c0 + chunk], s, n_iter=30)
+        np.testing.assert_array_equal(eh[c0:c0 + chunk], ec)
+        np.testing.assert_array_equal(ah[c0:c0 + chunk], ac)
+    e1, a1, st1, *_ = run_gpu(smf, torch, cube, s, n_iter=30)
+    print(assert_parity(eh, ah, e1.astype(np.float64), a1.astype(np.float64), "chunked vs whole"))
+
+
 def test_permutation_invariance(smf, torch):
     cfg = synth.scaled(synth.CONFIGS["segment"], cols=8)
     cube, s, _ = synth.generate(cfg)
