@@ -713,21 +713,21 @@ struct PilotArgs {
 __global__ void k0_pilot(PilotArgs a) {
     const int c = blockIdx.x, tid = threadIdx.x;
     __shared__ double cc;
+    __shared__ double scratch[32];
     const int np = min(kPilotRows, a.N);
     const size_t base = (size_t)c * a.N * a.B;
-    float v = 0.f;
-    if (tid < a.B) {
+    double sq = 0.0;
+    for (int b = tid; b < a.B; b += blockDim.x) {
         float sum = 0.f;
-        for (int p = 0; p < np; ++p) sum += a.L[base + (size_t)p * a.B + tid];
-        v = sum / (float)np;
-        a.pil32[(size_t)c * a.B + tid] = v;
+        for (int p = 0; p < np; ++p) sum += a.L[base + (size_t)p * a.B + b];
+        const float v = sum / (float)np;
+        a.pil32[(size_t)c * a.B + b] = v;
+        sq += (double)v * (double)v;
     }
-    double sq[1] = {(double)v * (double)v};
-    __shared__ double scratch[32];
     // block reduction (fixed order)
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sq[0] += __shfl_xor_sync(0xffffffffu, sq[0], off);
-    if ((tid & 31) == 0) scratch[tid >> 5] = sq[0];
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if ((tid & 31) == 0) scratch[tid >> 5] = sq;
     __syncthreads();
     if (tid == 0) {
         double t = 0.0;
@@ -735,7 +735,10 @@ __global__ void k0_pilot(PilotArgs a) {
         cc = t;
     }
     __syncthreads();
-    if (tid < a.B) a.ghat32[(size_t)c * a.B + tid] = cc > 0.0 ? (float)((double)v / cc) : 0.f;
+    for (int b = tid; b < a.B; b += blockDim.x) {
+        const float v = a.pil32[(size_t)c * a.B + b];
+        a.ghat32[(size_t)c * a.B + b] = cc > 0.0 ? (float)((double)v / cc) : 0.f;
+    }
 }
 
 // ---------------------------------------------------------------- shared column state

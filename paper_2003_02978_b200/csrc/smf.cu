@@ -18,6 +18,7 @@
 
 #include "../../include/smf.h"
 #include "kernels.cuh"
+#include "wide.cuh"
 
 using namespace smf;
 
@@ -114,6 +115,9 @@ struct Plan {
     // K1 (persistent, one CTA per SM, own tile height T1 and partition)
     int G1, S1, W1, T1, tpc1, NT1, be_full;
     bool k1tc;
+    // wide path (any B): K1w block grid, K3w tiles of kWideT3 pixels
+    bool wide;
+    int BEw, NBw, NGw;
     long long ttot1;
     size_t smem1, smem2, smem3;
     // workspace offsets
@@ -128,15 +132,18 @@ int stats_threads(int B);
 bool k1tc_fits(int B);
 int k1tc_be(int B);
 size_t k1tc_smem(int B);
+bool narrow(int B) { return B >= 4 && B <= 96 && B % 4 == 0; }
+int wide_blocks_per_sm(int B);
 
 bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     const int B = ctx->bands;
     p.cols = cols;
     p.N = N;
     p.B = B;
-    p.tpc = (N + kTileRows - 1) / kTileRows;
+    p.wide = !narrow(B);
+    p.tpc = (N + (p.wide ? kWideT3 : kTileRows) - 1) / (p.wide ? kWideT3 : kTileRows);
     p.ttot = (long long)cols * p.tpc;
-    const int per_sm = std::max(1, sweep_blocks_per_sm(B));
+    const int per_sm = std::max(1, p.wide ? wide_blocks_per_sm(B) : sweep_blocks_per_sm(B));
     long long G = (long long)ctx->sm_count * per_sm;
     if (G > p.ttot) G = p.ttot;
     p.G = (int)G;
@@ -146,7 +153,10 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
         if (t1 > t0) S = std::max(S, (int)((t1 - 1) / p.tpc - t0 / p.tpc + 1));
     }
     p.S = S;
-    p.k1tc = ctx->stats_kernel != SMF_STATS_FFMA && k1tc_fits(B);
+    p.BEw = (B + 2 + 7) / 8 * 8;
+    p.NBw = (p.BEw / 8) * (p.BEw / 8 + 1) / 2;
+    p.NGw = (p.NBw + kWideNT1 - 1) / kWideNT1;
+    p.k1tc = !p.wide && ctx->stats_kernel != SMF_STATS_FFMA && k1tc_fits(B);
     p.T1 = p.k1tc ? kTileTC : k1_rows(B);
     p.NT1 = p.k1tc ? K1TC<1>::NT : stats_threads(B);
     p.be_full = p.k1tc ? k1tc_be(B) : 0;
@@ -159,10 +169,16 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
         if (t1 > t0) p.S1 = std::max(p.S1, (int)((t1 - 1) / p.tpc1 - t0 / p.tpc1 + 1));
     }
     p.W1 = p.k1tc ? p.be_full * p.be_full : k1_width_host(B);
-    TileGeom g = TileGeom::make(B);
-    p.smem1 = p.k1tc ? k1tc_smem(B) : k1_smem(B);
-    p.smem2 = k2_init_smem(B, p.W1);
-    p.smem3 = (size_t)kStages * g.stage_bytes + 1024;
+    if (p.wide) {
+        p.smem1 = k1w_smem(B, p.BEw);
+        p.smem2 = k2w_init_smem(B);
+        p.smem3 = k3w_smem(B);
+    } else {
+        TileGeom g = TileGeom::make(B);
+        p.smem1 = p.k1tc ? k1tc_smem(B) : k1_smem(B);
+        p.smem2 = k2_init_smem(B, p.W1);
+        p.smem3 = (size_t)kStages * g.stage_bytes + 1024;
+    }
     size_t o = 0;
     auto take = [&](size_t bytes) {
         size_t r = o;
@@ -183,7 +199,7 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.o_status = take((size_t)cols * 4);
     p.o_pilot = take(cb * 4);
     p.o_ghat = take(cb * 4);
-    p.o_part1 = take((size_t)p.G1 * p.S1 * p.W1 * 8);
+    p.o_part1 = p.wide ? take((size_t)cols * p.NGw * kWideNT1 * 64 * 8) : take((size_t)p.G1 * p.S1 * p.W1 * 8);
     p.o_part3 = take((size_t)p.G * p.S * (B + 3) * 8);
     p.total = o;
     return true;
@@ -326,7 +342,22 @@ int sweep_blocks_per_sm(int B) {
     return std::max(n, 1);
 }
 
-bool supported(int B) { return B >= 4 && B <= 96 && B % 4 == 0; }
+int wide_blocks_per_sm(int B) {
+    const size_t smem = k3w_smem(B);
+    if (cudaFuncSetAttribute(k3w_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 0;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k3w_sweep, kWideNT3, smem) != cudaSuccess) return 0;
+    return n;
+}
+
+// narrow kernels for B % 4 == 0, B <= 96; the wide path for any other B whose K3w
+// tile (two buffers of kWideT3 rows) fits in shared memory
+bool supported(int B) {
+    if (narrow(B)) return true;
+    return B >= 1 && B <= kWideNT3 * kWideMaxBPT && k3w_smem(B) <= 220 * 1024 &&
+           k2w_init_smem(B) <= 200 * 1024 && k1w_smem(B, (B + 2 + 7) / 8 * 8) <= 220 * 1024;
+}
 
 CUresult make_maps(const float* rad, int cols, int N, int B, CUtensorMap* main_map, CUtensorMap* tail_map,
                    int rows = kTileRows) {
@@ -398,10 +429,12 @@ smf_status validate(smf_ctx* ctx, const void* rad, int cols, int pixels, const v
 smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned char* ws, cudaStream_t st,
                         double* mean_out, double* cov_out, int stats_only, int& launches) {
     CUtensorMap mm, tm;
-    CUresult cr = make_maps(rad, p.cols, p.N, p.B, &mm, &tm, p.T1);
-    if (cr != CUDA_SUCCESS) {
-        set_err(ctx, "cuTensorMapEncodeTiled (K1) failed (%d)", (int)cr);
-        return SMF_ERR_CUDA;
+    if (!p.wide) {
+        CUresult cr = make_maps(rad, p.cols, p.N, p.B, &mm, &tm, p.T1);
+        if (cr != CUDA_SUCCESS) {
+            set_err(ctx, "cuTensorMapEncodeTiled (K1) failed (%d)", (int)cr);
+            return SMF_ERR_CUDA;
+        }
     }
     PilotArgs pa;
     pa.L = rad;
@@ -417,6 +450,52 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k0_pilot launch");
     ++launches;
+    if (p.wide) {
+        WideStatsArgs wa;
+        wa.L = rad;
+        wa.pil32 = pa.pil32;
+        wa.ghat32 = pa.ghat32;
+        wa.part = (double*)(ws + p.o_part1);
+        wa.cols = p.cols;
+        wa.N = p.N;
+        wa.B = p.B;
+        wa.BE = p.BEw;
+        wa.NB = p.NBw;
+        wa.NG = p.NGw;
+        e = cudaFuncSetAttribute(k1w_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats smem attribute");
+        {
+            ProfScope ps(ctx, st, SMF_KERNEL_STATS);
+            k1w_stats<<<dim3(p.NGw, p.cols), kWideNT1, p.smem1, st>>>(wa);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats launch");
+        ++launches;
+        WideInitArgs ia;
+        ia.cs = col_state(p, ws, ctx->s_dev);
+        ia.pil32 = pa.pil32;
+        ia.part = wa.part;
+        ia.mean_out = mean_out;
+        ia.cov_out = cov_out;
+        ia.cols = p.cols;
+        ia.N = p.N;
+        ia.B = p.B;
+        ia.BE = p.BEw;
+        ia.NG = p.NGw;
+        ia.use_albedo = ctx->use_albedo;
+        ia.stats_only = stats_only;
+        ia.ridge_rel = ctx->ridge;
+        e = cudaFuncSetAttribute(k2w_init, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem2);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init smem attribute");
+        {
+            ProfScope ps(ctx, st, SMF_KERNEL_INIT);
+            k2w_init<<<p.cols, kWideNT2, p.smem2, st>>>(ia);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init launch");
+        ++launches;
+        return SMF_OK;
+    }
     StatsArgs sa;
     sa.pil32 = pa.pil32;
     sa.ghat32 = pa.ghat32;
@@ -629,10 +708,12 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     Plan p;
     make_plan(ctx, cols, pixels, p);
     CUtensorMap mm, tm;
-    CUresult cr = make_maps(radiance, cols, pixels, ctx->bands, &mm, &tm);
-    if (cr != CUDA_SUCCESS) {
-        set_err(ctx, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
-        return SMF_ERR_CUDA;
+    if (!p.wide) {
+        CUresult cr = make_maps(radiance, cols, pixels, ctx->bands, &mm, &tm);
+        if (cr != CUDA_SUCCESS) {
+            set_err(ctx, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+            return SMF_ERR_CUDA;
+        }
     }
     unsigned char* ws = (unsigned char*)workspace;
     int launches = 0;
@@ -670,27 +751,38 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     ua.G = p.G;
     ua.S = p.S;
     ua.ttot = p.ttot;
-    cudaError_t e0 = cudaFuncSetAttribute(k2_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(p.B * p.B * 8));
+    const size_t smem_up = p.wide ? k2w_update_smem(p.B) : (size_t)p.B * p.B * 8;
+    void* ufn = p.wide ? reinterpret_cast<void*>(&k2w_update) : reinterpret_cast<void*>(&k2_update);
+    cudaError_t e0 = cudaFuncSetAttribute(ufn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_up);
     if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k2_update smem attribute");
-    void* kfn = sweep_kernel(p.B);
+    void* kfn = p.wide ? reinterpret_cast<void*>(&k3w_sweep) : sweep_kernel(p.B);
     e0 = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem3);
     if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k3_sweep smem attribute");
     for (int k = 0; k <= ctx->n_iter; ++k) {
         if (k > 0) {
             {
                 ProfScope ps(ctx, st, SMF_KERNEL_UPDATE);
-                k2_update<<<cols, 128, (size_t)p.B * p.B * 8, st>>>(ua);
+                if (p.wide)
+                    k2w_update<<<cols, kWideNT2, smem_up, st>>>(ua);
+                else
+                    k2_update<<<cols, 128, smem_up, st>>>(ua);
             }
             e0 = cudaGetLastError();
             if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k2_update launch");
             ++launches;
         }
         sa.k = k;
-        void* args[] = {(void*)&mm, (void*)&tm, (void*)&sa};
         cudaError_t e;
         {
             ProfScope ps(ctx, st, SMF_KERNEL_SWEEP);
-            e = cudaLaunchKernel(kfn, dim3(p.G), dim3(kTileRows), args, p.smem3, st);
+            if (p.wide) {
+                const float* rad = radiance;
+                void* args[] = {(void*)&sa, (void*)&rad};
+                e = cudaLaunchKernel(kfn, dim3(p.G), dim3(kWideNT3), args, p.smem3, st);
+            } else {
+                void* args[] = {(void*)&mm, (void*)&tm, (void*)&sa};
+                e = cudaLaunchKernel(kfn, dim3(p.G), dim3(kTileRows), args, p.smem3, st);
+            }
         }
         if (e != cudaSuccess) return cuda_fail(ctx, e, "sweep launch");
         ++launches;

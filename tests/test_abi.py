@@ -53,6 +53,7 @@ def test_host_side_calls_without_gpu(lib):
     assert L.smf_status_string(0) == b"SMF_OK"
     assert L.smf_status_string(4) == b"SMF_ERR_NUMERICAL"
     assert smf.supported_bands(72) and smf.supported_bands(32)
+    assert smf.supported_bands(425) and smf.supported_bands(5)   # wide path
     assert not smf.supported_bands(0)
     h = ctypes.c_void_p()
     assert L.smf_create(None, 72) == smf.SMF_ERR_INVALID_ARGUMENT

@@ -172,6 +172,48 @@ def test_ragged_shapes(smf, torch, cols, pixels, bands):
     print(assert_parity(enh, alb, a_ref, r_ref, f"{cols}x{pixels}x{bands}"))
 
 
+# ------------------------------------------------------------------ wide path (any band count)
+@pytest.mark.parametrize("cols,pixels,bands", [(2, 300, 5), (3, 257, 13), (2, 700, 101), (1, 130, 98),
+                                               (2, 1200, 425)])
+def test_wide_bands(smf, torch, cols, pixels, bands):
+    """Band counts outside the narrow kernels (B % 4 != 0 or B > 96) run the wide path
+    (k1w_stats / k2w_init / k2w_update / k3w_sweep)."""
+    cfg = synth.scaled(synth.CONFIGS["tiny"], cols=cols, pixels=pixels, bands=bands, rank=min(8, bands))
+    cube, s, _ = synth.generate(cfg)
+    kw = dict(n_iter=6, ridge_rel=1e-3 if pixels <= bands else 0.0)
+    enh, alb, st, mu, q, nl = run_gpu(smf, torch, cube, s, **kw)
+    a_ref, r_ref, st_ref = oracle.retrieve(cube, s, **oracle_kw(kw))
+    np.testing.assert_array_equal(st, st_ref)
+    print(assert_parity(enh, alb, a_ref, r_ref, f"wide {cols}x{pixels}x{bands}"))
+
+
+def test_wide_initial_statistics(smf, torch):
+    cfg = synth.scaled(synth.CONFIGS["stress"], cols=2)
+    cube, s, _ = synth.generate(cfg, columns=[0, 1])
+    r = smf.Retriever(cfg.bands, s)
+    mean, cov = r.initial_statistics(torch.from_numpy(cube).cuda())
+    mean, cov = mean.cpu().numpy(), cov.cpu().numpy()
+    for c in range(2):
+        C_ref = oracle.covariance(cube[c])
+        np.testing.assert_allclose(mean[c], oracle.mean(cube[c]), rtol=1e-6)
+        scale = np.sqrt(np.outer(np.diag(C_ref), np.diag(C_ref)))
+        assert (np.abs(cov[c] - C_ref) / scale).max() < 1e-5
+
+
+def test_stress_columns_parity(smf, torch):
+    """BASELINE.json configs[3] (598 x 4000 x 425, 30 iterations): sampled columns,
+    including plume columns, against the oracle."""
+    cfg = synth.CONFIGS["stress"]
+    cols = _plume_columns(cfg, k=3, extra=2, seed=2)
+    cube, s, _ = synth.generate(cfg, columns=cols)
+    enh, alb, st, mu, q, _ = run_gpu(smf, torch, cube, s, n_iter=cfg.n_iter)
+    a_ref, r_ref, st_ref = oracle.retrieve(cube, s, n_iter=cfg.n_iter)
+    assert (st == 0).all() and (st_ref == 0).all()
+    rep = assert_parity(enh, alb, a_ref, r_ref, "stress")
+    print(rep)
+    assert rep["zero_set_agreement"] > 0.999
+
+
 def test_column_status_codes(smf, torch):
     cfg = synth.scaled(synth.CONFIGS["tiny"], cols=5)
     cube, s, _ = synth.generate(cfg)
