@@ -342,12 +342,25 @@ int sweep_blocks_per_sm(int B) {
     return std::max(n, 1);
 }
 
+void* wide_sweep_kernel(int B) {
+    switch (k3w_j(B)) {
+        case 2: return reinterpret_cast<void*>(&k3w_sweep<2>);
+        case 4: return reinterpret_cast<void*>(&k3w_sweep<4>);
+        case 8: return reinterpret_cast<void*>(&k3w_sweep<8>);
+        case 14: return reinterpret_cast<void*>(&k3w_sweep<14>);
+        case 20: return reinterpret_cast<void*>(&k3w_sweep<20>);
+        case 28: return reinterpret_cast<void*>(&k3w_sweep<28>);
+        default: return nullptr;
+    }
+}
+
 int wide_blocks_per_sm(int B) {
+    void* fn = wide_sweep_kernel(B);
+    if (!fn) return 0;
     const size_t smem = k3w_smem(B);
-    if (cudaFuncSetAttribute(k3w_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return 0;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k3w_sweep, kWideNT3, smem) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kWideNT3, smem) != cudaSuccess) return 0;
     return n;
 }
 
@@ -355,7 +368,7 @@ int wide_blocks_per_sm(int B) {
 // tile (two buffers of kWideT3 rows) fits in shared memory
 bool supported(int B) {
     if (narrow(B)) return true;
-    return B >= 1 && B <= kWideNT3 * kWideMaxBPT && k3w_smem(B) <= 220 * 1024 &&
+    return B >= 1 && k3w_j(B) > 0 && k3w_smem(B) <= 220 * 1024 &&
            k2w_init_smem(B) <= 200 * 1024 && k1w_smem(B, (B + 2 + 7) / 8 * 8) <= 220 * 1024;
 }
 
@@ -755,7 +768,7 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     void* ufn = p.wide ? reinterpret_cast<void*>(&k2w_update) : reinterpret_cast<void*>(&k2_update);
     cudaError_t e0 = cudaFuncSetAttribute(ufn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_up);
     if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k2_update smem attribute");
-    void* kfn = p.wide ? reinterpret_cast<void*>(&k3w_sweep) : sweep_kernel(p.B);
+    void* kfn = p.wide ? wide_sweep_kernel(p.B) : sweep_kernel(p.B);
     e0 = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem3);
     if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k3_sweep smem attribute");
     for (int k = 0; k <= ctx->n_iter; ++k) {

@@ -62,8 +62,8 @@ __device__ __forceinline__ void cp_async_floats(float* dst, const float* src, in
 __device__ __forceinline__ int wide_tile_shift(const float* src) { return (int)(((uintptr_t)src & 15) >> 2); }
 
 // ---------------------------------------------------------------- K1w
-constexpr int kWideT1 = 32;      // pixels per K1w shared tile
-constexpr int kWideNT1 = 128;    // threads (= 8x8 blocks) per K1w CTA
+constexpr int kWideT1 = 30;      // pixels per K1w shared tile (two tiles + pilot fit 2 CTAs/SM)
+constexpr int kWideNT1 = 256;    // threads (= 8x8 blocks) per K1w CTA
 constexpr int kWideRun1 = 16;    // K1w tiles per fp32 run before the fp64 fold
 
 struct WideStatsArgs {
@@ -74,58 +74,111 @@ struct WideStatsArgs {
     int cols, N, B, BE, NB, NG;
 };
 
-__host__ inline size_t k1w_smem(int B, int BE) { return ((size_t)kWideT1 * BE + 2 * (size_t)B) * 4 + 16; }
+__host__ inline size_t k1w_smem(int B, int BE) { return (2 * (size_t)kWideT1 * BE + 2 * (size_t)B) * 4 + 16; }
 
+// One CTA per (block group g, column c): the column's pixel rows arrive by cp.async
+// straight into the extended-row layout of a double-buffered tile (row stride BE),
+// are turned into extended rows in place (warp per 4 pixels, interleaved), and feed
+// 128 8x8 FFMA register blocks.
 __global__ void __launch_bounds__(kWideNT1, 2) k1w_stats(WideStatsArgs a) {
     extern __shared__ __align__(16) float w1_smem[];
-    float* ext = w1_smem;                       // [kWideT1][BE]
-    float* pil = ext + kWideT1 * a.BE;          // [B]
-    float* gh = pil + a.B;                      // [B]
+    float* ext = w1_smem;                          // [2][kWideT1][BE]
+    float* pil = ext + 2 * kWideT1 * a.BE;         // [B]
+    float* gh = pil + a.B;                         // [B]
     const int g = blockIdx.x, c = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int B = a.B, BE = a.BE;
     const int blk = g * kWideNT1 + tid;
     const bool active = blk < a.NB;
     int R = 0, C = 0;
     if (active) blk_rc(blk, R, C);
-    for (int b = tid; b < a.B; b += kWideNT1) {
-        pil[b] = a.pil32[(size_t)c * a.B + b];
-        gh[b] = a.ghat32[(size_t)c * a.B + b];
+    for (int b = tid; b < B; b += kWideNT1) {
+        pil[b] = a.pil32[(size_t)c * B + b];
+        gh[b] = a.ghat32[(size_t)c * B + b];
     }
-    const float* Lc = a.L + (size_t)c * a.N * a.B;
+    const float* Lc = a.L + (size_t)c * a.N * B;
+    const int ntile = (a.N + kWideT1 - 1) / kWideT1;
+    auto load_tile = [&](int t) {
+        const int p0 = t * kWideT1, rows = min(kWideT1, a.N - p0);
+        float* buf = ext + (t & 1) * kWideT1 * BE;
+        const uint32_t d0 = smem_u32(buf);
+        const float* src = Lc + (size_t)p0 * B;
+        for (int r = 0; r < rows; ++r)
+            for (int b = tid; b < B; b += kWideNT1) cp_async4(d0 + 4 * (r * BE + b), src + (size_t)r * B + b);
+        cp_async_commit();
+    };
+    load_tile(0);
+    // fp32 register runs are folded into this thread's fp64 partial block in global
+    // memory (L2-resident, 512 B per thread), keeping registers for the FFMA tile
+    double* out = a.part + ((size_t)c * a.NG * kWideNT1 + blk) * 64;
     float acc[64];
-    double acc64[64];
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-        acc[i] = 0.f;
-        acc64[i] = 0.0;
-    }
+    for (int i = 0; i < 64; ++i) acc[i] = 0.f;
     int run = 0;
-    for (int p0 = 0; p0 < a.N; p0 += kWideT1) {
-        __syncthreads();   // previous tile consumed (and pil/gh loaded)
-        // extended rows: warp w takes pixels w, w + 4, ...; sigma = L . ghat (fixed order)
-        for (int pp = wid; pp < kWideT1; pp += kWideNT1 / 32) {
-            const int p = p0 + pp;
-            float* row = ext + pp * a.BE;
-            if (p < a.N) {
-                const float* Lp = Lc + (size_t)p * a.B;
-                float sg = 0.f;
-                for (int b = lane; b < a.B; b += 32) sg = fmaf(__ldg(Lp + b), gh[b], sg);
-                sg = warp_sum_f(sg);
-                for (int b = lane; b < a.B; b += 32) row[b] = fmaf(-sg, pil[b], __ldg(Lp + b));
-                for (int b = a.B + lane; b < a.BE; b += 32) row[b] = b == a.B ? sg - 1.f : (b == a.B + 1 ? 1.f : 0.f);
-            } else {
-                for (int b = lane; b < a.BE; b += 32) row[b] = 0.f;
+    bool first_fold = true;
+    auto fold = [&]() {
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                out[i] = (first_fold ? 0.0 : out[i]) + (double)acc[i];
+                acc[i] = 0.f;
+            }
+        }
+        first_fold = false;
+    };
+    for (int t = 0; t < ntile; ++t) {
+        const int p0 = t * kWideT1, rows = min(kWideT1, a.N - p0);
+        float* buf = ext + (t & 1) * kWideT1 * BE;
+        __syncthreads();                       // buffer (t+1)&1 no longer read by anyone
+        if (t + 1 < ntile) {
+            load_tile(t + 1);
+            cp_async_wait_1();
+        } else {
+            cp_async_wait_all();
+        }
+        __syncthreads();                       // tile t landed
+        // extended rows in place: x = L - sigma c, rho = sigma - 1, 1, zero pad; a warp
+        // per 8 pixels, their sigma dot products interleaved
+        {
+            constexpr int PW = (kWideT1 + kWideNT1 / 32 - 1) / (kWideNT1 / 32);   // pixels per warp
+            const int pp0 = wid * PW;
+            float sg[PW];
+#pragma unroll
+            for (int u = 0; u < PW; ++u) sg[u] = 0.f;
+            for (int b = lane; b < B; b += 32) {
+                const float gb = gh[b];
+#pragma unroll
+                for (int u = 0; u < PW; ++u)
+                    if (pp0 + u < rows) sg[u] = fmaf(buf[(pp0 + u) * BE + b], gb, sg[u]);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                for (int u = 0; u < PW; ++u) sg[u] += __shfl_xor_sync(0xffffffffu, sg[u], off);
+            for (int b = lane; b < BE; b += 32) {
+                const float pb = b < B ? pil[b] : 0.f;
+#pragma unroll
+                for (int u = 0; u < PW; ++u) {
+                    const int pp = pp0 + u;
+                    if (pp >= kWideT1) break;
+                    float* row = buf + pp * BE;
+                    float v;
+                    if (pp >= rows) v = 0.f;
+                    else if (b < B) v = fmaf(-sg[u], pb, row[b]);
+                    else v = b == B ? sg[u] - 1.f : (b == B + 1 ? 1.f : 0.f);
+                    row[b] = v;
+                }
             }
         }
         __syncthreads();
         if (active) {
-            const float* ra = ext + R * 8;
-            const float* rb = ext + C * 8;
-#pragma unroll 2
+            const float* ra = buf + R * 8;
+            const float* rb = buf + C * 8;
+#pragma unroll 3
             for (int pp = 0; pp < kWideT1; ++pp) {
-                const float4 a0 = *reinterpret_cast<const float4*>(ra + pp * a.BE);
-                const float4 a1 = *reinterpret_cast<const float4*>(ra + pp * a.BE + 4);
-                const float4 b0 = *reinterpret_cast<const float4*>(rb + pp * a.BE);
-                const float4 b1 = *reinterpret_cast<const float4*>(rb + pp * a.BE + 4);
+                const float4 a0 = *reinterpret_cast<const float4*>(ra + pp * BE);
+                const float4 a1 = *reinterpret_cast<const float4*>(ra + pp * BE + 4);
+                const float4 b0 = *reinterpret_cast<const float4*>(rb + pp * BE);
+                const float4 b1 = *reinterpret_cast<const float4*>(rb + pp * BE + 4);
                 const float xa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                 const float xb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
@@ -135,19 +188,11 @@ __global__ void __launch_bounds__(kWideNT1, 2) k1w_stats(WideStatsArgs a) {
             }
         }
         if (++run == kWideRun1) {
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-                acc64[i] += (double)acc[i];
-                acc[i] = 0.f;
-            }
+            fold();
             run = 0;
         }
     }
-    if (active) {
-        double* out = a.part + ((size_t)c * a.NG * kWideNT1 + blk) * 64;
-#pragma unroll
-        for (int i = 0; i < 64; ++i) out[i] = acc64[i] + (double)acc[i];
-    }
+    if (run > 0 || first_fold) fold();
 }
 
 // ---------------------------------------------------------------- K2w init
@@ -165,33 +210,36 @@ struct WideInitArgs {
     double ridge_rel;
 };
 
-__host__ inline size_t k2w_init_smem(int B) { return (size_t)(5 * B + kGJ * kGJ + 32 * 4) * 8; }
+__host__ inline size_t k2w_init_smem(int B) { return (size_t)(5 * B + kGJ * kGJ + (size_t)B * (kGJ + 1) + 32 * 4) * 8; }
 
 // In-place blocked Gauss-Jordan inverse of the SPD matrix A (B x B, row-major, global)
-// by one CTA: for every diagonal block K, D = A_KK^-1 (shared memory, unblocked GJ),
-// R = D A_K* (row panel), A_ij -= A_iK R_Kj, A_iK = -A_iK D, A_KK = D. No pivoting: for
-// an SPD matrix the pivots are the Cholesky pivots squared; a pivot <= tol flags NOT_SPD.
-__device__ bool wide_gj_inverse(double* A, int B, double tol, double* D /* [kGJ][kGJ] smem */) {
+// by one CTA: for every diagonal block K (kGJ wide), D = A_KK^-1 (shared memory,
+// unblocked GJ), R = D A_K* (row panel), A_ij -= A_iK R_Kj, A_iK = -A_iK D, A_KK = D.
+// The old column panel A_.K is staged in shared memory (Cp, row stride kGJ + 1) and
+// read as broadcasts by the thread-per-column trailing update; the new row panel stays
+// in registers. No pivoting: for an SPD matrix the pivots are the Cholesky pivots
+// squared; a pivot <= tol flags NOT_SPD.
+__device__ bool wide_gj_inverse(double* A, int B, double tol, double* D /* [kGJ][kGJ] */,
+                                double* Cp /* [B][kGJ + 1] */) {
+    constexpr int CS = kGJ + 1;
     const int tid = threadIdx.x, nt = blockDim.x;
-    __shared__ int sh_bad;
-    if (tid == 0) sh_bad = 0;
-    __syncthreads();
     for (int k0 = 0; k0 < B; k0 += kGJ) {
         const int nb = min(kGJ, B - k0);
-        // (a) D = inverse of the diagonal block (unblocked GJ in shared memory, zero-padded)
-        for (int e = tid; e < kGJ * kGJ; e += nt) D[e] = 0.0;
+        // stage D (zero-padded) and the column panel
+        for (int e = tid; e < kGJ * kGJ; e += nt) {
+            const int r = e / kGJ, cc = e % kGJ;
+            D[e] = (r < nb && cc < nb) ? A[(size_t)(k0 + r) * B + k0 + cc] : 0.0;
+        }
+        for (int e = tid; e < B * kGJ; e += nt) {
+            const int r = e / kGJ, cc = e % kGJ;
+            Cp[r * CS + cc] = cc < nb ? A[(size_t)r * B + k0 + cc] : 0.0;
+        }
         __syncthreads();
-        for (int e = tid; e < nb * nb; e += nt) D[(e / nb) * kGJ + e % nb] = A[(size_t)(k0 + e / nb) * B + k0 + e % nb];
-        __syncthreads();
+        // (a) D = inverse of the diagonal block (unblocked GJ)
         for (int j = 0; j < nb; ++j) {
             const double piv = D[j * kGJ + j];
-            if (!(piv > tol) || !isfinite(piv)) {
-                if (tid == 0) sh_bad = 1;
-                __syncthreads();
-                return false;
-            }
+            if (!(piv > tol) || !isfinite(piv)) return false;   // uniform: D is shared
             const double p = 1.0 / piv;
-            // rank-1 update of the other entries, then row / column j
             for (int e = tid; e < nb * nb; e += nt) {
                 const int r = e / nb, cc = e % nb;
                 if (r != j && cc != j) D[r * kGJ + cc] -= D[r * kGJ + j] * p * D[j * kGJ + cc];
@@ -207,53 +255,66 @@ __device__ bool wide_gj_inverse(double* A, int B, double tol, double* D /* [kGJ]
             if (tid == 0) D[j * kGJ + j] = p;
             __syncthreads();
         }
-        // (b) row panel R_Kj = D A_Kj and (c) trailing update A_ij -= A_iK R_Kj for
-        // i, j outside the block: thread per column j, R_.j kept in registers; the old
-        // column panel A_iK (same for every thread) is read through L1 as broadcasts
+        // (b) row panel R_Kj = D A_Kj and (c) trailing update A_ij -= A_iK R_Kj, thread per
+        // column j outside the block
         for (int j = tid; j < B; j += nt) {
             if (j >= k0 && j < k0 + nb) continue;
-            double rp[kGJ];
-#pragma unroll
-            for (int s2 = 0; s2 < kGJ; ++s2) rp[s2] = s2 < nb ? A[(size_t)(k0 + s2) * B + j] : 0.0;
             double rn[kGJ];
+            {
+                double rp[kGJ];
 #pragma unroll
-            for (int r = 0; r < kGJ; ++r) {
-                double v = 0.0;
+                for (int s2 = 0; s2 < kGJ; ++s2) rp[s2] = s2 < nb ? A[(size_t)(k0 + s2) * B + j] : 0.0;
 #pragma unroll
-                for (int s2 = 0; s2 < kGJ; ++s2) v = fma(D[r * kGJ + s2], rp[s2], v);   // D is zero-padded
-                rn[r] = v;
+                for (int r = 0; r < kGJ; ++r) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int s2 = 0; s2 < kGJ; ++s2) v = fma(D[r * kGJ + s2], rp[s2], v);
+                    rn[r] = v;
+                }
             }
 #pragma unroll
             for (int r = 0; r < kGJ; ++r)
                 if (r < nb) A[(size_t)(k0 + r) * B + j] = rn[r];
-            for (int i = 0; i < B; ++i) {
-                if (i >= k0 && i < k0 + nb) continue;
-                const double* Ai = A + (size_t)i * B + k0;
-                double v = A[(size_t)i * B + j];
+            // rows in groups of 8 so that 8 global loads are in flight per thread
+            for (int i0 = 0; i0 < B; i0 += 8) {
+                double v[8];
 #pragma unroll
-                for (int s2 = 0; s2 < kGJ; ++s2) v = fma(-(s2 < nb ? Ai[s2] : 0.0), rn[s2], v);
-                A[(size_t)i * B + j] = v;
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u;
+                    v[u] = (i < B && (i < k0 || i >= k0 + nb)) ? A[(size_t)i * B + j] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u;
+                    if (i >= B) break;
+                    if (i >= k0 && i < k0 + nb) continue;
+                    const double* ci = Cp + i * CS;
+                    double w0 = v[u], w1 = 0.0;
+#pragma unroll
+                    for (int s2 = 0; s2 < kGJ; s2 += 2) {
+                        w0 = fma(-ci[s2], rn[s2], w0);
+                        w1 = fma(-ci[s2 + 1], rn[s2 + 1], w1);
+                    }
+                    A[(size_t)i * B + j] = w0 + w1;
+                }
             }
         }
-        __syncthreads();
-        // (d) column panel A_iK = -A_iK D, (e) A_KK = D
+        // (d) column panel A_iK = -A_iK D (from the staged old panel), (e) A_KK = D
         for (int i = tid; i < B; i += nt) {
             if (i >= k0 && i < k0 + nb) continue;
-            double row[kGJ];
-#pragma unroll
-            for (int s2 = 0; s2 < kGJ; ++s2) row[s2] = s2 < nb ? A[(size_t)i * B + k0 + s2] : 0.0;
-#pragma unroll
-            for (int r = 0; r < kGJ; ++r) {
+            const double* ci = Cp + i * CS;
+#pragma unroll 4
+            for (int r = 0; r < nb; ++r) {
                 double v = 0.0;
 #pragma unroll
-                for (int s2 = 0; s2 < kGJ; ++s2) v = fma(row[s2], D[s2 * kGJ + r], v);
-                if (r < nb) A[(size_t)i * B + k0 + r] = -v;
+                for (int s2 = 0; s2 < kGJ; ++s2) v = fma(ci[s2], D[s2 * kGJ + r], v);
+                A[(size_t)i * B + k0 + r] = -v;
             }
         }
         for (int e = tid; e < nb * nb; e += nt) A[(size_t)(k0 + e / nb) * B + k0 + e % nb] = D[(e / nb) * kGJ + e % nb];
         __syncthreads();
     }
-    return sh_bad == 0;
+    return true;
 }
 
 __global__ void __launch_bounds__(kWideNT2) k2w_init(WideInitArgs a) {
@@ -265,7 +326,8 @@ __global__ void __launch_bounds__(kWideNT2) k2w_init(WideInitArgs a) {
     double* vt = cv + B;         // [B] t0
     double* mh = vt + B;         // [B] fp32 mhat (as double)
     double* D = mh + B;          // [kGJ][kGJ]
-    double* scratch = D + kGJ * kGJ;   // [32][4]
+    double* Cp = D + kGJ * kGJ;        // [B][kGJ + 1] column panel
+    double* scratch = Cp + (size_t)B * (kGJ + 1);   // [32][4]
     __shared__ int bad;
     __shared__ double sh_tol, sh_mm;
     const double invN = 1.0 / (double)a.N;
@@ -328,7 +390,7 @@ __global__ void __launch_bounds__(kWideNT2) k2w_init(WideInitArgs a) {
         __syncthreads();
     }
     int st = bad;
-    if (st == COL_OK && !wide_gj_inverse(A, B, sh_tol, D)) st = COL_NOT_SPD;
+    if (st == COL_OK && !wide_gj_inverse(A, B, sh_tol, D, Cp)) st = COL_NOT_SPD;
     __syncthreads();
     const double mm = sh_mm;
     for (int b = tid; b < B; b += nt) {
@@ -341,7 +403,15 @@ __global__ void __launch_bounds__(kWideNT2) k2w_init(WideInitArgs a) {
     double qc[3] = {0.0, 0.0, 0.0};
     for (int b = tid; b < B; b += nt) {
         double y = 0.0;
-        for (int i = 0; i < B; ++i) y = fma(A[(size_t)i * B + b], vt[i], y);
+        int i = 0;
+        for (; i + 8 <= B; i += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = A[(size_t)(i + u) * B + b];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) y = fma(v[u], vt[i + u], y);
+        }
+        for (; i < B; ++i) y = fma(A[(size_t)i * B + b], vt[i], y);
         const float z32 = (float)y;
         a.cs.z32[(size_t)c * B + b] = z32;
         a.cs.tprev[(size_t)c * B + b] = vt[b];
@@ -426,8 +496,18 @@ __global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
         const int j = tid + jj * nt;
         if (j >= B) break;
         double yt = 0.0, yh = 0.0;
-#pragma unroll 4
-        for (int i = 0; i < B; ++i) {
+        int i = 0;
+        for (; i + 16 <= B; i += 16) {   // 16 independent loads in flight
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = __ldg(Ainv + (size_t)(i + u) * B + j);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                yt = fma(v[u], sh_t[i + u], yt);
+                yh = fma(v[u], sh_h[i + u], yh);
+            }
+        }
+        for (; i < B; ++i) {
             const double v = __ldg(Ainv + (size_t)i * B + j);
             yt = fma(v, sh_t[i], yt);
             yh = fma(v, sh_h[i], yh);
@@ -497,20 +577,36 @@ __global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
 
 // ---------------------------------------------------------------- K3w sweep
 constexpr int kWideT3 = 32;       // pixels per K3w tile
-constexpr int kWideNT3 = 256;     // threads per K3w CTA (8 warps, 4 pixels each)
+constexpr int kWideNT3 = 256;     // threads per K3w CTA (8 warps)
 constexpr int kWideMaxBPT = 8;    // bands per thread in the beta L' accumulation (B <= 2048)
 
-__host__ inline size_t k3w_tile_floats(int B) { return ((size_t)kWideT3 * B + 4 + 3) / 4 * 4; }
-__host__ inline size_t k3w_smem(int B) { return (2 * k3w_tile_floats(B) + 2 * (size_t)B) * 4 + 16; }
+// floats per tile buffer: 32 rows + 4 floats of alignment shift + 32 floats of zero pad
+// (the register pass reads up to 32 J - B floats past a row; the pad keeps that finite)
+__host__ __device__ inline size_t k3w_tile_floats(int B) { return ((size_t)kWideT3 * B + 4 + 32 + 3) / 4 * 4; }
+__host__ inline int k3w_j(int B) {
+    const int j = (B + 31) / 32;
+    return j <= 2 ? 2 : j <= 4 ? 4 : j <= 8 ? 8 : j <= 14 ? 14 : j <= 20 ? 20 : j <= 28 ? 28 : 0;
+}
+__host__ inline size_t k3w_smem(int B) {
+    const int J = k3w_j(B);
+    return (2 * k3w_tile_floats(B) + 2 * (size_t)(J > 0 ? 32 * J : B)) * 4 + 16;
+}
 
-__global__ void __launch_bounds__(kWideNT3, 1) k3w_sweep(SweepArgs a, const float* L) {
+// J = elements per lane of a pixel row (B <= 32 J); each warp processes PB pixels at
+// once (their dot products interleaved for ILP), keeping the row in registers between
+// the albedo pass and the projection pass.
+template <int J>
+__global__ void __launch_bounds__(kWideNT3, 2) k3w_sweep(SweepArgs a, const float* L) {
+    constexpr int PB = J <= 14 ? 4 : 2;
+    constexpr int NBT = (32 * J + kWideNT3 - 1) / kWideNT3;   // bands per thread in phase B
     extern __shared__ __align__(16) float w4_smem[];
     const int B = a.B, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const size_t TF = ((size_t)kWideT3 * B + 4 + 3) / 4 * 4;   // floats per tile buffer (+ shift room)
+    const size_t TF = k3w_tile_floats(B);
     float* buf0 = w4_smem;
-    float* zs = w4_smem + 2 * TF;      // [B]
-    float* ms = zs + B;                // [B]
-    __shared__ float sh_beta[kWideT3], sh_sc[kWideT3];
+    float* zs = w4_smem + 2 * TF;      // [32 J], zero beyond B
+    float* ms = zs + 32 * J;           // [32 J], zero beyond B
+    __shared__ float2 sh_bs[kWideT3];   // (beta, sc) per pixel of the tile
+    __shared__ float sh_aprev[kWideT3];
     __shared__ float sh_par[4];
     __shared__ int sh_st;
     __shared__ double red[kWideNT3 / 32][3];
@@ -518,9 +614,10 @@ __global__ void __launch_bounds__(kWideNT3, 1) k3w_sweep(SweepArgs a, const floa
     const int ntl = (int)(te - tb);
     const int cfirst = (int)(tb / a.tpc);
     const bool accum = a.k < a.n_iter;
-    const int nbt = (B + kWideNT3 - 1) / kWideNT3;   // bands per thread (<= kWideMaxBPT)
+    // zero both buffers once: the pads past the tile data stay zero
+    for (size_t e = tid; e < 2 * TF; e += kWideNT3) buf0[e] = 0.f;
+    __syncthreads();
 
-    // tile i -> shared buffer i % 2, shifted to the source's 16-byte phase
     auto tile_src = [&](long long gt, int& rows) -> const float* {
         const int c = (int)(gt / a.tpc), tt = (int)(gt - (long long)c * a.tpc);
         const int p0 = tt * kWideT3;
@@ -536,18 +633,17 @@ __global__ void __launch_bounds__(kWideNT3, 1) k3w_sweep(SweepArgs a, const floa
     };
     if (ntl > 0) load_tile(0);
 
-    float acc[kWideMaxBPT];
+    float acc[NBT];
 #pragma unroll
-    for (int j = 0; j < kWideMaxBPT; ++j) acc[j] = 0.f;
-    float sb = 0.f, sb2 = 0.f, sbs = 0.f;   // per-thread partials (thread 0.. of the beta loop)
+    for (int j = 0; j < NBT; ++j) acc[j] = 0.f;
+    float sb = 0.f, sb2 = 0.f, sbs = 0.f;
 
     auto flush = [&](int slot) {
-        // band sums: thread j owns bands j, j + NT, ...; scalar sums reduced over the CTA
         double* P = a.part3 + ((size_t)blockIdx.x * a.S + slot) * (B + 3);
 #pragma unroll
-        for (int j = 0; j < kWideMaxBPT; ++j) {
+        for (int j = 0; j < NBT; ++j) {
             const int b = tid + j * kWideNT3;
-            if (j < nbt && b < B) P[3 + b] = (double)acc[j];
+            if (b < B) P[3 + b] = (double)acc[j];
             acc[j] = 0.f;
         }
         float v3[3] = {sb, sb2, sbs};
@@ -576,9 +672,9 @@ __global__ void __launch_bounds__(kWideNT3, 1) k3w_sweep(SweepArgs a, const floa
         if (i + 1 < ntl) load_tile(i + 1);
         if (c != cur) {
             if (cur >= 0 && accum) flush(cur - cfirst);
-            for (int b = tid; b < B; b += kWideNT3) {
-                zs[b] = a.z32[(size_t)c * B + b];
-                ms[b] = a.mhat32[(size_t)c * B + b];
+            for (int b = tid; b < 32 * J; b += kWideNT3) {
+                zs[b] = b < B ? a.z32[(size_t)c * B + b] : 0.f;
+                ms[b] = b < B ? a.mhat32[(size_t)c * B + b] : 0.f;
             }
             if (tid == 0) {
                 sh_par[0] = a.kc32[2 * c];
@@ -602,71 +698,114 @@ __global__ void __launch_bounds__(kWideNT3, 1) k3w_sweep(SweepArgs a, const floa
             cst = sh_st;
             cur = c;
         }
+        // previous alpha of this tile's pixels (reweighting term, Eq. 5), off the critical path
+        if (tid < kWideT3)
+            sh_aprev[tid] = (a.k > 0 && a.use_sparsity && cst == COL_OK && tid < rows)
+                                ? a.enh[(size_t)c * a.N + p0 + tid] : 0.f;
         if (i + 1 < ntl) cp_async_wait_1(); else cp_async_wait_all();
-        __syncthreads();   // tile i landed for every thread
-        int rr;
-        const float* T = buf0 + (i & 1) * TF + wide_tile_shift(tile_src(tb + i, rr));
-        // ---- phase A: warp per pixel (albedo, projection, update)
-        for (int pp = wid; pp < kWideT3; pp += kWideNT3 / 32) {
-            float beta = 0.f, sc = 0.f;
-            if (pp < rows) {
-                const size_t pix = (size_t)c * a.N + p0 + pp;
-                if (cst != COL_OK) {
-                    if (lane == 0) {
-                        a.enh[pix] = __int_as_float(0x7fc00000);
-                        a.alb[pix] = __int_as_float(0x7fc00000);
-                    }
-                } else {
-                    const float* row = T + (size_t)pp * B;
-                    float r = 0.f;
-                    for (int b = lane; b < B; b += 32) r = fmaf(row[b], ms[b], r);
-                    r = warp_sum_f(r);                       // albedo factor (Eq. 7)
-                    sc = r * mmf;
-                    float dz = 0.f;
-                    for (int b = lane; b < B; b += 32) dz = fmaf(fmaf(-sc, ms[b], row[b]), zs[b], dz);
-                    dz = warp_sum_f(dz);
-                    const float pz = dz + fmaf(sc, mz, -cz);  // (L - mu^k).z
-                    const float rr2 = a.use_albedo ? r : 1.f;
-                    const float rt = a.use_albedo ? fmaxf(r, a.r_floor) : 1.f;
-                    float out;
-                    if (a.k == 0) {
-                        const float a0 = pz / (rt * q);
-                        out = a.n_iter == 0 ? a0 : (a0 > 0.f ? a0 : 0.f);
-                    } else {
-                        const float aprev = a.use_sparsity ? a.enh[pix] : 0.f;
-                        const float w = a.use_sparsity ? 1.f / (aprev + a.eps) : 0.f;
-                        const float x = (pz - w) / (rt * q);
-                        out = x > 0.f ? x : 0.f;
-                    }
-                    __syncwarp();
-                    if (lane == 0) {
-                        a.enh[pix] = out;
-                        if (a.k == 0) a.alb[pix] = rr2;
-                    }
-                    beta = rt * out;
+        __syncthreads();   // tile i and sh_aprev visible to every thread
+        int rr_;
+        const float* T = buf0 + (i & 1) * TF + wide_tile_shift(tile_src(tb + i, rr_));
+        // ---- phase A: a warp per PB pixels (albedo, projection, update)
+        for (int base = wid * PB; base < kWideT3; base += (kWideNT3 / 32) * PB) {
+            float v[PB][J], r[PB], dz[PB];
+#pragma unroll
+            for (int pb = 0; pb < PB; ++pb) {
+                r[pb] = 0.f;
+                const float* row = T + (size_t)(base + pb) * B;
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    v[pb][j] = row[lane + 32 * j];
+                    r[pb] = fmaf(v[pb][j], ms[lane + 32 * j], r[pb]);
                 }
             }
-            if (lane == 0) {
-                sh_beta[pp] = beta;
-                sh_sc[pp] = sc;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                for (int pb = 0; pb < PB; ++pb) r[pb] += __shfl_xor_sync(0xffffffffu, r[pb], off);
+#pragma unroll
+            for (int pb = 0; pb < PB; ++pb) {
+                const float sc = r[pb] * mmf;    // albedo-centred radiance L' = L - sc mhat
+                dz[pb] = 0.f;
+#pragma unroll
+                for (int j = 0; j < J; ++j)
+                    dz[pb] = fmaf(fmaf(-sc, ms[lane + 32 * j], v[pb][j]), zs[lane + 32 * j], dz[pb]);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                for (int pb = 0; pb < PB; ++pb) dz[pb] += __shfl_xor_sync(0xffffffffu, dz[pb], off);
+            // lane pb finishes pixel base + pb
+#pragma unroll
+            for (int pb = 0; pb < PB; ++pb) {
+                if (lane != pb) continue;
+                const int pp = base + pb;
+                float beta = 0.f, sc = 0.f;
+                if (pp < rows) {
+                    const size_t pix = (size_t)c * a.N + p0 + pp;
+                    if (cst != COL_OK) {
+                        a.enh[pix] = __int_as_float(0x7fc00000);
+                        a.alb[pix] = __int_as_float(0x7fc00000);
+                    } else {
+                        const float r0 = r[pb];                     // albedo factor (Eq. 7)
+                        sc = r0 * mmf;
+                        const float pz = dz[pb] + fmaf(sc, mz, -cz);  // (L - mu^k).z
+                        const float rt = a.use_albedo ? fmaxf(r0, a.r_floor) : 1.f;
+                        float out;
+                        if (a.k == 0) {
+                            const float a0 = pz / (rt * q);                       // line 6
+                            out = a.n_iter == 0 ? a0 : (a0 > 0.f ? a0 : 0.f);     // reading C3
+                            a.alb[pix] = a.use_albedo ? r0 : 1.f;
+                        } else {
+                            const float w = a.use_sparsity ? 1.f / (sh_aprev[pp] + a.eps) : 0.f;   // Eq. 5
+                            const float x = (pz - w) / (rt * q);                                  // line 16
+                            out = x > 0.f ? x : 0.f;                                              // C14
+                        }
+                        a.enh[pix] = out;
+                        beta = rt * out;
+                    }
+                }
+                sh_bs[pp] = make_float2(beta, sc);
                 sb += beta;
                 sb2 = fmaf(beta, beta, sb2);
                 sbs = fmaf(beta, sc, sbs);
             }
         }
         __syncthreads();
-        // ---- phase B: sum beta L' with a thread per band
+        // ---- phase B: sum beta L' with a thread per band (NBT bands per thread, the
+        // (beta, sc) pair of each pixel loaded once for all of them)
         if (accum && cst == COL_OK) {
+            float mbv[NBT];
+            const float* tcol[NBT];
 #pragma unroll
-            for (int j = 0; j < kWideMaxBPT; ++j) {
+            for (int j = 0; j < NBT; ++j) {
                 const int b = tid + j * kWideNT3;
-                if (j < nbt && b < B) {
-                    const float mb = ms[b];
-                    float s = acc[j];
-                    for (int pp = 0; pp < rows; ++pp) s = fmaf(sh_beta[pp], fmaf(-sh_sc[pp], mb, T[(size_t)pp * B + b]), s);
-                    acc[j] = s;
+                mbv[j] = b < B ? ms[b] : 0.f;
+                tcol[j] = T + (b < B ? b : 0);
+            }
+            float s0[NBT], s1[NBT];
+#pragma unroll
+            for (int j = 0; j < NBT; ++j) {
+                s0[j] = acc[j];
+                s1[j] = 0.f;
+            }
+            int pp = 0;
+            for (; pp + 2 <= rows; pp += 2) {
+                const float2 bs0 = sh_bs[pp], bs1 = sh_bs[pp + 1];
+#pragma unroll
+                for (int j = 0; j < NBT; ++j) {
+                    s0[j] = fmaf(bs0.x, fmaf(-bs0.y, mbv[j], tcol[j][(size_t)pp * B]), s0[j]);
+                    s1[j] = fmaf(bs1.x, fmaf(-bs1.y, mbv[j], tcol[j][(size_t)(pp + 1) * B]), s1[j]);
                 }
             }
+            if (pp < rows) {
+                const float2 bs0 = sh_bs[pp];
+#pragma unroll
+                for (int j = 0; j < NBT; ++j) s0[j] = fmaf(bs0.x, fmaf(-bs0.y, mbv[j], tcol[j][(size_t)pp * B]), s0[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < NBT; ++j)
+                if (tid + j * kWideNT3 < B) acc[j] = s0[j] + s1[j];
         }
         __syncthreads();   // buffer i & 1 free for tile i + 2
     }
