@@ -502,7 +502,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init smem attribute");
         {
             ProfScope ps(ctx, st, SMF_KERNEL_INIT);
-            k2w_init<<<p.cols, kWideNT2, p.smem2, st>>>(ia);
+            k2w_init<<<p.cols, std::min(kWideNTI, (p.B + 31) / 32 * 32), p.smem2, st>>>(ia);
         }
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init launch");

@@ -39,6 +39,8 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+// K3w ring: at most S - 1 newer groups may stay pending
+__device__ __forceinline__ void cp_async_wait_ring() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // Copy n contiguous floats global -> shared with cp.async: 16-byte pieces where
 // source and destination share the same alignment phase, 4-byte pieces otherwise.
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(kWideNT1, 2) k1w_stats(WideStatsArgs a) {
 
 // ---------------------------------------------------------------- K2w init
 constexpr int kWideNT2 = 256;
+constexpr int kWideNTI = 512;     // k2w_init: a thread per matrix column (B <= 512) in the GJ updates
 constexpr int kWideMaxBPT2 = 8;   // bands per thread in k2w_update (B <= 2048)
 constexpr int kGJ = 32;          // Gauss-Jordan block size
 
@@ -317,7 +320,7 @@ __device__ bool wide_gj_inverse(double* A, int B, double tol, double* D /* [kGJ]
     return true;
 }
 
-__global__ void __launch_bounds__(kWideNT2) k2w_init(WideInitArgs a) {
+__global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     extern __shared__ double w2_smem[];
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x, nt = blockDim.x;
     double* dm = w2_smem;        // [B] mean(L) - c, later mu0
@@ -576,8 +579,9 @@ __global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
 }
 
 // ---------------------------------------------------------------- K3w sweep
-constexpr int kWideT3 = 32;       // pixels per K3w tile
-constexpr int kWideNT3 = 256;     // threads per K3w CTA (8 warps)
+constexpr int kWideT3 = 16;       // pixels per K3w tile
+constexpr int kWideS3 = 2;        // K3w cp.async ring depth (tiles in flight)
+constexpr int kWideNT3 = 128;     // threads per K3w CTA (4 warps; 4 CTAs per SM)
 constexpr int kWideMaxBPT = 8;    // bands per thread in the beta L' accumulation (B <= 2048)
 
 // floats per tile buffer: 32 rows + 4 floats of alignment shift + 32 floats of zero pad
@@ -589,21 +593,21 @@ __host__ inline int k3w_j(int B) {
 }
 __host__ inline size_t k3w_smem(int B) {
     const int J = k3w_j(B);
-    return (2 * k3w_tile_floats(B) + 2 * (size_t)(J > 0 ? 32 * J : B)) * 4 + 16;
+    return (kWideS3 * k3w_tile_floats(B) + 2 * (size_t)(J > 0 ? 32 * J : B)) * 4 + 16;
 }
 
 // J = elements per lane of a pixel row (B <= 32 J); each warp processes PB pixels at
 // once (their dot products interleaved for ILP), keeping the row in registers between
 // the albedo pass and the projection pass.
 template <int J>
-__global__ void __launch_bounds__(kWideNT3, 2) k3w_sweep(SweepArgs a, const float* L) {
-    constexpr int PB = J <= 14 ? 4 : 2;
+__global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const float* L) {
+    constexpr int PB = kWideT3 / (kWideNT3 / 32);   // pixels per warp per tile
     constexpr int NBT = (32 * J + kWideNT3 - 1) / kWideNT3;   // bands per thread in phase B
     extern __shared__ __align__(16) float w4_smem[];
     const int B = a.B, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const size_t TF = k3w_tile_floats(B);
     float* buf0 = w4_smem;
-    float* zs = w4_smem + 2 * TF;      // [32 J], zero beyond B
+    float* zs = w4_smem + kWideS3 * TF;   // [32 J], zero beyond B
     float* ms = zs + 32 * J;           // [32 J], zero beyond B
     __shared__ float2 sh_bs[kWideT3];   // (beta, sc) per pixel of the tile
     __shared__ float sh_aprev[kWideT3];
@@ -614,8 +618,8 @@ __global__ void __launch_bounds__(kWideNT3, 2) k3w_sweep(SweepArgs a, const floa
     const int ntl = (int)(te - tb);
     const int cfirst = (int)(tb / a.tpc);
     const bool accum = a.k < a.n_iter;
-    // zero both buffers once: the pads past the tile data stay zero
-    for (size_t e = tid; e < 2 * TF; e += kWideNT3) buf0[e] = 0.f;
+    // zero the ring once: the pads past the tile data stay zero
+    for (size_t e = tid; e < kWideS3 * TF; e += kWideNT3) buf0[e] = 0.f;
     __syncthreads();
 
     auto tile_src = [&](long long gt, int& rows) -> const float* {
@@ -627,11 +631,14 @@ __global__ void __launch_bounds__(kWideNT3, 2) k3w_sweep(SweepArgs a, const floa
     auto load_tile = [&](int i) {
         int rows;
         const float* src = tile_src(tb + i, rows);
-        float* dst = buf0 + (i & 1) * TF + wide_tile_shift(src);
+        float* dst = buf0 + (i % kWideS3) * TF + wide_tile_shift(src);
         cp_async_floats(dst, src, rows * B, tid, kWideNT3);
-        cp_async_commit();
     };
-    if (ntl > 0) load_tile(0);
+    // prologue: tiles 0 .. S-2 in flight (one commit group per tile, empty groups past the end)
+    for (int i = 0; i < kWideS3 - 1; ++i) {
+        if (i < ntl) load_tile(i);
+        cp_async_commit();
+    }
 
     float acc[NBT];
 #pragma unroll
@@ -669,7 +676,9 @@ __global__ void __launch_bounds__(kWideNT3, 2) k3w_sweep(SweepArgs a, const floa
         const int c = ccur.c;
         const int p0 = ccur.tt * kWideT3;
         const int rows = min(kWideT3, a.N - p0);
-        if (i + 1 < ntl) load_tile(i + 1);
+        // refill: tile i + S - 1 into the slot freed by tile i - 1 (end-of-tile barrier)
+        if (i + kWideS3 - 1 < ntl) load_tile(i + kWideS3 - 1);
+        cp_async_commit();
         if (c != cur) {
             if (cur >= 0 && accum) flush(cur - cfirst);
             for (int b = tid; b < 32 * J; b += kWideNT3) {
@@ -702,10 +711,10 @@ __global__ void __launch_bounds__(kWideNT3, 2) k3w_sweep(SweepArgs a, const floa
         if (tid < kWideT3)
             sh_aprev[tid] = (a.k > 0 && a.use_sparsity && cst == COL_OK && tid < rows)
                                 ? a.enh[(size_t)c * a.N + p0 + tid] : 0.f;
-        if (i + 1 < ntl) cp_async_wait_1(); else cp_async_wait_all();
-        __syncthreads();   // tile i and sh_aprev visible to every thread
+        cp_async_wait_ring();   // this thread's copies of tile i have landed
+        __syncthreads();        // ... and everyone's; sh_aprev visible
         int rr_;
-        const float* T = buf0 + (i & 1) * TF + wide_tile_shift(tile_src(tb + i, rr_));
+        const float* T = buf0 + (i % kWideS3) * TF + wide_tile_shift(tile_src(tb + i, rr_));
         // ---- phase A: a warp per PB pixels (albedo, projection, update)
         for (int base = wid * PB; base < kWideT3; base += (kWideNT3 / 32) * PB) {
             float v[PB][J], r[PB], dz[PB];
@@ -807,7 +816,7 @@ __global__ void __launch_bounds__(kWideNT3, 2) k3w_sweep(SweepArgs a, const floa
             for (int j = 0; j < NBT; ++j)
                 if (tid + j * kWideNT3 < B) acc[j] = s0[j] + s1[j];
         }
-        __syncthreads();   // buffer i & 1 free for tile i + 2
+        __syncthreads();   // slot i % S free for tile i + S
     }
     if (cur >= 0 && accum) flush(cur - cfirst);
 }
