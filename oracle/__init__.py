@@ -39,7 +39,8 @@ _i64 = ctypes.POINTER(ctypes.c_int64)
 
 
 class _Diag(ctypes.Structure):
-    _fields_ = [("mu", _d), ("cov", _d), ("q", _d), ("alpha_hist", _d), ("nnz", _i64), ("rho", _d)]
+    _fields_ = [("mu", _d), ("cov", _d), ("q", _d), ("alpha_hist", _d), ("nnz", _i64), ("rho", _d),
+                ("energy", _d)]
 
 
 def build(force: bool = False) -> str:
@@ -85,6 +86,8 @@ def lib():
                                       ctypes.c_double, _d, _d, _i32, ctypes.c_int]
         L.oracle_retrieve.restype = ctypes.c_int
         L.oracle_max_threads.restype = ctypes.c_int
+        L.oracle_energy.argtypes = [ctypes.c_int, ctypes.c_int, _d, _d, _d, ctypes.c_double, _d, _d, _d, _d]
+        L.oracle_energy.restype = ctypes.c_double
     return _lib
 
 
@@ -162,6 +165,16 @@ DEFAULTS = dict(n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2, lambda_
                 r_floor=0.05)
 
 
+def energy(L, mu, C, t, alpha, rt, w=None, rho=0.0):
+    """Eq. 8 as printed: sum_i d_i^T (C+rho I)^-1 d_i + r~_i w_i |alpha_i|,
+    d_i = L_i - r~_i alpha_i t - mu (fp64; NaN if C + rho I is not SPD)."""
+    L, mu, C, t, alpha, rt = map(_c64, (L, mu, C, t, alpha, rt))
+    N, B = L.shape
+    wp = _p(_c64(w), _d) if w is not None else None
+    return lib().oracle_energy(N, B, _p(L, _d), _p(mu, _d), _p(C, _d), float(rho), _p(t, _d),
+                               _p(alpha, _d), _p(rt, _d), wp)
+
+
 def retrieve_column(L, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2,
                     lambda_rel=0.0, r_floor=0.05, diagnostics=False):
     """One partition. L fp32 [N][B]. Returns (alpha, r, status[, diag dict])."""
@@ -175,9 +188,11 @@ def retrieve_column(L, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-
     if diagnostics:
         K = n_iter + 1
         out = dict(mu=np.zeros((K, B)), cov=np.zeros((K, B, B)), q=np.zeros(K),
-                   alpha_hist=np.zeros((K, N)), nnz=np.zeros(K, dtype=np.int64), rho=np.zeros(1))
+                   alpha_hist=np.zeros((K, N)), nnz=np.zeros(K, dtype=np.int64), rho=np.zeros(1),
+                   energy=np.zeros(K))
         dg = _Diag(_p(out["mu"], _d), _p(out["cov"], _d), _p(out["q"], _d),
-                   _p(out["alpha_hist"], _d), _p(out["nnz"], _i64), _p(out["rho"], _d))
+                   _p(out["alpha_hist"], _d), _p(out["nnz"], _i64), _p(out["rho"], _d),
+                   _p(out["energy"], _d))
     rc = lib().oracle_retrieve_column(_p(L, _f), N, B, _p(s, _f), int(n_iter), int(use_sparsity),
                                       int(use_albedo), float(eps), float(lambda_rel),
                                       float(r_floor), _p(alpha, _d), _p(r, _d),

@@ -169,10 +169,43 @@ typedef struct {
     double* alpha_hist;  /* [n_iter+1][N]  alpha^k (k=0: unclamped alpha0)      */
     int64_t* nnz;        /* [n_iter+1]     # alpha^k > 0                        */
     double* rho;         /* [1]                                                  */
+    double* energy;      /* [n_iter+1]     Eq. 8 at iteration k (see below)      */
 } oracle_diag;
 
 static void nan_fill(int N, double* alpha, double* r) {
     for (int i = 0; i < N; ++i) { alpha[i] = NAN; r[i] = NAN; }
+}
+
+/* Eq. 8, the objective tracked in Fig. 4, as printed (no 1/2,
+ * cf. reading C4): E = sum_i d_i^T (C + rho I)^-1 d_i + sum_i r~_i w_i alpha_i with
+ * d_i = L_i - r~_i alpha_i t - mu. Per pixel: forward substitution with this file's
+ * Cholesky factor G of C + rho I, so d^T (C+rho I)^-1 d = |G^-1 d|^2. w may be NULL
+ * (w = 0). Returns NaN if C + rho I is not SPD. */
+double oracle_energy(int N, int B, const double* L, const double* mu, const double* C, double rho,
+                     const double* t, const double* alpha, const double* rt, const double* w) {
+    double* G = (double*)malloc(sizeof(double) * (size_t)B * B);
+    double* d = (double*)malloc(sizeof(double) * B);
+    double* y = (double*)malloc(sizeof(double) * B);
+    double E = NAN;
+    if (!G || !d || !y) goto out;
+    for (int a = 0; a < B * B; ++a) G[a] = C[a];
+    for (int b = 0; b < B; ++b) G[(size_t)b * B + b] += rho;
+    if (oracle_cholesky(B, G) != OR_OK) goto out;
+    E = 0.0;
+    for (int i = 0; i < N; ++i) {
+        for (int b = 0; b < B; ++b) d[b] = L[(size_t)i * B + b] - rt[i] * alpha[i] * t[b] - mu[b];
+        double q = 0.0;
+        for (int r = 0; r < B; ++r) {           /* y = G^-1 d (lower triangular) */
+            double v = d[r];
+            for (int c = 0; c < r; ++c) v -= G[(size_t)r * B + c] * y[c];
+            y[r] = v / G[(size_t)r * B + r];
+            q += y[r] * y[r];
+        }
+        E += q + (w ? rt[i] * w[i] * fabs(alpha[i]) : 0.0);
+    }
+out:
+    free(G); free(d); free(y);
+    return E;
 }
 
 /* One partition (column). L: fp32 [N][B] row-major (promoted to fp64).
@@ -243,9 +276,13 @@ int oracle_retrieve_column(const float* Lf, int N, int B, const float* sf, int n
         if (dg->alpha_hist) memcpy(dg->alpha_hist, alpha, sizeof(double) * N);
         if (dg->nnz) dg->nnz[0] = nz;
     }
+    if (n_iter > 0)
+        for (int i = 0; i < N; ++i) alpha[i] = alpha[i] > 0.0 ? alpha[i] : 0.0;   /* reading C3 */
+    /* energy trace (reading C19): E_k = Eq. 8 with the statistics mu^k, C^k, t^k and the
+     * weights w^k of iteration k, at the updated alpha^k (alpha0 as stored; w^0 = 0) */
+    if (dg && dg->energy) dg->energy[0] = oracle_energy(N, B, L, mu, C, rho, t, alpha, rt, NULL);
     if (n_iter == 0) goto done;                               /* unclamped alpha0 */
 
-    for (int i = 0; i < N; ++i) alpha[i] = alpha[i] > 0.0 ? alpha[i] : 0.0;   /* reading C3 */
     memcpy(mu_prev, mu, sizeof(double) * B);
 
     for (int k = 1; k <= n_iter; ++k) {
@@ -282,6 +319,7 @@ int oracle_retrieve_column(const float* Lf, int N, int B, const float* sf, int n
             if (dg->q) dg->q[k] = q;
             if (dg->alpha_hist) memcpy(dg->alpha_hist + (size_t)k * N, alpha, sizeof(double) * N);
             if (dg->nnz) dg->nnz[k] = nz;
+            if (dg->energy) dg->energy[k] = oracle_energy(N, B, L, mu, C, rho, t, alpha, rt, w);
         }
         memcpy(mu_prev, mu, sizeof(double) * B);
     }

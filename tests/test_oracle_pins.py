@@ -321,3 +321,15 @@ def test_r_floor_reading_c10(oracle_lib):
     a1, r1, rc = oracle_lib.retrieve_column(L, s, n_iter=0, use_sparsity=0, use_albedo=0)
     assert r[7] < 0
     assert a[7] == pytest.approx(a1[7] / 0.05, rel=1e-12)
+
+
+def test_p6_energy_converges(oracle_lib):
+    """P6 sanity (not a pin): the Eq. 8 energy settles -- the paper reports stable
+    convergence within 20 iterations; SPEC AC6 asks |E30 - E20| <= 1 %."""
+    from paper_2003_02978_b200 import synth
+    cfg = synth.CONFIGS["segment"]
+    cube, s, _ = synth.generate(cfg, columns=[int(np.flatnonzero(synth.plume_field(cfg).any(axis=1))[0])])
+    a, r, rc, dg = oracle_lib.retrieve_column(cube[0], s, n_iter=30, diagnostics=True)
+    E = dg["energy"]
+    assert rc == 0 and np.isfinite(E).all()
+    assert abs(E[30] - E[20]) <= 0.01 * abs(E[30])

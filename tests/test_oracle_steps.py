@@ -134,3 +134,71 @@ def test_closed_form_is_gls_estimate(oracle_lib):
     for i in range(N):
         sol, *_ = scipy.linalg.lstsq((W @ t)[:, None], W @ (L[i] - mu))
         assert a[i] == pytest.approx(sol[0], rel=1e-10, abs=1e-12)
+
+
+# ---- energy, Eq. 8, the objective of Fig. 4 ----------------
+def test_energy_closed_form_NB(oracle_lib):
+    """alpha = 0, w = 0 with mu, C the sample mean / population covariance: the
+    quadratic term is sum_i (L_i-mu)^T C^-1 (L_i-mu) = N tr(C^-1 C) = N B exactly."""
+    rng = np.random.default_rng(11)
+    N, B = 40, 5
+    L = rng.normal(size=(N, B)) @ rng.normal(size=(B, B)) + 3.0
+    mu = L.mean(axis=0)
+    C = (L - mu).T @ (L - mu) / N
+    E = oracle_lib.energy(L, mu, C, np.ones(B), np.zeros(N), np.ones(N))
+    assert abs(E - N * B) < 1e-9 * N * B
+
+
+def test_energy_exact_fit_and_penalty(oracle_lib):
+    """L_i = mu + r~_i alpha_i t makes every residual d_i zero: E is then
+    the penalty sum_i r~_i w_i |alpha_i| alone."""
+    rng = np.random.default_rng(12)
+    N, B = 12, 4
+    mu, t = rng.uniform(1, 2, B), -rng.uniform(0.1, 0.2, B)
+    alpha, rt, w = rng.uniform(0, 5, N), rng.uniform(0.5, 1.5, N), rng.uniform(0, 2, N)
+    L = mu + (rt * alpha)[:, None] * t
+    A = rng.normal(size=(B, B))
+    C = A @ A.T + B * np.eye(B)
+    assert abs(oracle_lib.energy(L, mu, C, t, alpha, rt)) < 1e-20
+    E = oracle_lib.energy(L, mu, C, t, alpha, rt, w)
+    assert abs(E - np.sum(rt * w * alpha)) < 1e-12 * np.sum(rt * w * alpha)
+
+
+def test_energy_matches_direct_sum(oracle_lib):
+    """Random 10-pixel instance vs the term-by-term sum with numpy's inverse."""
+    rng = np.random.default_rng(13)
+    N, B = 10, 3
+    L, mu, t = rng.normal(size=(N, B)), rng.normal(size=B), rng.normal(size=B)
+    alpha, rt, w = rng.uniform(-1, 3, N), rng.uniform(0.5, 1.5, N), rng.uniform(0, 1, N)
+    A = rng.normal(size=(B, B))
+    C, rho = A @ A.T + 0.1 * np.eye(B), 0.3
+    Ci = np.linalg.inv(C + rho * np.eye(B))
+    d = L - (rt * alpha)[:, None] * t - mu
+    ref = np.einsum("ib,bc,ic->", d, Ci, d) + np.sum(rt * w * np.abs(alpha))
+    assert abs(oracle_lib.energy(L, mu, C, t, alpha, rt, w, rho) - ref) < 1e-10 * abs(ref)
+
+
+def test_energy_trace_wiring(oracle_lib):
+    """The retrieval's energy trace E_k (reading C19) equals Eq. 8 evaluated with the
+    iteration's own mu^k, C^k (+ rho), t^k = mu^k (.) s, w^k = 1/(alpha^{k-1} + eps) and
+    the updated alpha^k (alpha^0 clamped when N_iter >= 1, w^0 = 0)."""
+    from paper_2003_02978_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS["tiny"], cols=1, pixels=300, bands=8, rank=4)
+    cube, s, _ = synth.generate(cfg)
+    L = cube[0].astype(np.float64)
+    eps, lam, K = 1e-2, 1e-3, 4
+    a, r, rc, dg = oracle_lib.retrieve_column(cube[0], s, n_iter=K, eps=eps, lambda_rel=lam,
+                                              diagnostics=True)
+    assert rc == 0
+    rt = np.maximum(r, 0.05)
+    rho = dg["rho"][0]
+    prev = None
+    for k in range(K + 1):
+        alpha = dg["alpha_hist"][k]
+        if k == 0:
+            alpha = np.maximum(alpha, 0.0)
+        t = dg["mu"][k] * s.astype(np.float64)
+        w = None if k == 0 else 1.0 / (prev + eps)
+        E = oracle_lib.energy(L, dg["mu"][k], dg["cov"][k], t, alpha, rt, w, rho)
+        assert abs(E - dg["energy"][k]) <= 1e-12 * abs(E)
+        prev = alpha
