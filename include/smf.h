@@ -163,6 +163,23 @@ enum { SMF_STATS_AUTO = 0, SMF_STATS_FFMA = 1, SMF_STATS_TENSOR = 2 };
 smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind);
 int smf_stats_kernel_used(const smf_ctx* ctx);
 
+/* Energy trace (the objective of Eq. 8, tracked over the iterations in
+ * Fig. 4). When enabled, smf_retrieve also records per column and per
+ * iteration k = 0..N_iter
+ *   E_k = sum_i d_i^T (C^k + rho I)^-1 d_i + sum_i r~_i w_i^k |alpha_i^k|,
+ *   d_i = L_i - r~_i alpha_i^k t^k - mu^k
+ * with the statistics mu^k, C^k, t^k and the weights w^k of iteration k at the updated
+ * alpha^k (alpha0 as stored, w^0 = 0; reading C19). It is assembled exactly
+ * from per-column sufficient statistics (no per-pixel whitening): two more sums in the
+ * sweep and a rank-3 Woodbury trace, plus one small kernel launch per sweep.
+ * smf_energy_trace copies the trace of the last smf_retrieve that used `workspace`
+ * (device fp64 [N_iter + 1][cols], NaN for failed columns) to energy_out, enqueued on
+ * `stream`; SMF_ERR_NOT_CONFIGURED if the trace was not enabled. The workspace size
+ * depends on this switch and N_iter (query smf_workspace_bytes after setting them). */
+smf_status smf_set_energy_trace(smf_ctx* ctx, int enable);
+smf_status smf_energy_trace(smf_ctx* ctx, const void* workspace, int cols, int pixels, double* energy_out,
+                            void* stream);
+
 /* Kernel launches enqueued by the last smf_retrieve call on this context. */
 int smf_last_launch_count(const smf_ctx* ctx);
 

@@ -755,6 +755,11 @@ struct ColState {
     float* q32;       // [cols]
     int* status;      // [cols]
     const float* s;   // [B] unit absorption spectrum
+    // energy trace (Eq. 8, reading C19): per column tr((C0+rho I)^-1), rho, and
+    // T_k = tr((C^k+rho I)^-1 C0) + bbar^2 t'^T (C^k+rho I)^-1 t' of the current iteration
+    double* tra;      // [cols]
+    double* rho64;    // [cols]
+    double* tq;       // [cols]
 };
 
 // Deterministic block reduction of NV values per thread (fixed order).
@@ -899,6 +904,7 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
             amax = fmax(amax, A[b * B + b]);
         }
         sh_tol = (double)B * 2.220446049250313e-16 * amax;
+        a.cs.rho64[c] = rho;
     }
     {
         double mm_loc[1] = {0.0};
@@ -974,19 +980,99 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
         a.cs.kc32[2 * c] = (float)qc[1];
         a.cs.kc32[2 * c + 1] = (float)qc[2];
         a.cs.status[c] = st;
+        double tra = 0.0;   // tr((C0 + rho I)^-1) for the energy trace
+        for (int b = 0; b < B; ++b) tra += A[b * B + b];
+        a.cs.tra[c] = tra;
+        a.cs.tq[c] = (double)B - a.cs.rho64[c] * tra;
     }
 }
 
 // ---------------------------------------------------------------- K2 update
-// K3 partial layout per (CTA, column slot), fp64, width B + 3:
-//   [0] sum beta, [1] sum beta^2, [2] sum beta s, [3 + b] sum beta L'_b
-// with s_i = r_i |mu0|^2 (as fp32) and L'_i = L_i - s_i mhat (albedo-centred radiance).
+// K3 partial layout per (CTA, column slot), fp64, width B + 5 (kPartExtra past the bands):
+//   [0] sum beta, [1] sum beta^2, [2] sum beta s, [3 + b] sum beta L'_b,
+//   [B + 3] sum beta p, [B + 4] sum r~ w alpha   (energy trace only)
+// with s_i = r_i |mu0|^2 (as fp32), L'_i = L_i - s_i mhat (albedo-centred radiance) and
+// p_i = (L_i - mu^k).z^k the whitened projection of the sweep.
+constexpr int kPartExtra = 5;   // K3 partial width = B + kPartExtra
+
 struct UpdateArgs {
     ColState cs;
-    const double* part3;   // [G][S][B+3]
-    int cols, N, B, tpc, G, S;
+    const double* part3;   // [G][S][B+5]
+    double* energy;        // k_energy: [n_iter+1][cols]
+    int cols, N, B, tpc, G, S, k;
     long long ttot;
 };
+
+// Woodbury pieces shared by the narrow and wide updates: with U = [t', t, h],
+// Y = A0^-1 U, G = U^T Y, YY = Y^T Y and M the rank-3 coefficient matrix,
+// W = M (I + G M)^-1 so that (C^k + rho I)^-1 = A0^-1 - Y W Y^T.
+// Returns T_k = tr((C^k+rho I)^-1 C0) + bbar^2 t'^T (C^k+rho I)^-1 t' (energy trace).
+__device__ inline double woodbury_trace(const double M[3][3], const double* gv, const double* yy, int B,
+                                        double rho, double tra, double bbar) {
+    // (I + G M) and its inverse (3x3 adjugate)
+    double P[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double v = (i == j) ? 1.0 : 0.0;
+            for (int l = 0; l < 3; ++l) v += gv[i * 3 + l] * M[l][j];
+            P[i][j] = v;
+        }
+    const double det = P[0][0] * (P[1][1] * P[2][2] - P[1][2] * P[2][1]) -
+                       P[0][1] * (P[1][0] * P[2][2] - P[1][2] * P[2][0]) +
+                       P[0][2] * (P[1][0] * P[2][1] - P[1][1] * P[2][0]);
+    double Pi[3][3];
+    Pi[0][0] = (P[1][1] * P[2][2] - P[1][2] * P[2][1]) / det;
+    Pi[0][1] = (P[0][2] * P[2][1] - P[0][1] * P[2][2]) / det;
+    Pi[0][2] = (P[0][1] * P[1][2] - P[0][2] * P[1][1]) / det;
+    Pi[1][0] = (P[1][2] * P[2][0] - P[1][0] * P[2][2]) / det;
+    Pi[1][1] = (P[0][0] * P[2][2] - P[0][2] * P[2][0]) / det;
+    Pi[1][2] = (P[0][2] * P[1][0] - P[0][0] * P[1][2]) / det;
+    Pi[2][0] = (P[1][0] * P[2][1] - P[1][1] * P[2][0]) / det;
+    Pi[2][1] = (P[0][1] * P[2][0] - P[0][0] * P[2][1]) / det;
+    Pi[2][2] = (P[0][0] * P[1][1] - P[0][1] * P[1][0]) / det;
+    double W[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double v = 0.0;
+            for (int l = 0; l < 3; ++l) v += M[i][l] * Pi[l][j];
+            W[i][j] = v;
+        }
+    // tr(W G), tr(W YY), (G W G)_00
+    double trWG = 0.0, trWY = 0.0, gwg = 0.0;
+    for (int i = 0; i < 3; ++i)
+        for (int l = 0; l < 3; ++l) {
+            trWG += W[i][l] * gv[l * 3 + i];
+            trWY += W[i][l] * yy[l * 3 + i];
+            gwg += gv[0 * 3 + i] * W[i][l] * gv[l * 3 + 0];
+        }
+    return (double)B - trWG - rho * (tra - trWY) + bbar * bbar * (gv[0] - gwg);
+}
+
+// Energy of iteration k per column (Eq. 8, reading C19), after sweep k:
+//   E_k = N T_k - 2 sum beta p + q sum beta^2 + sum r~ w alpha.
+__global__ void k_energy(UpdateArgs a) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.cols) return;
+    double* out = a.energy + (size_t)a.k * a.cols + c;
+    if (a.cs.status[c] != COL_OK) {
+        *out = __longlong_as_double(0x7ff8000000000000ULL);
+        return;
+    }
+    const long long c0 = (long long)c * a.tpc, c1 = c0 + a.tpc;
+    int b0 = (int)((c0 * a.G) / a.ttot);
+    while (b0 > 0 && tile_begin(b0, a.ttot, a.G) > c0) --b0;
+    while (tile_begin(b0 + 1, a.ttot, a.G) <= c0) ++b0;
+    const int W = a.B + kPartExtra;
+    double s2 = 0.0, sbp = 0.0, swa = 0.0;
+    for (int b = b0; b < a.G && tile_begin(b, a.ttot, a.G) < c1; ++b) {
+        const int slot = c - (int)(tile_begin(b, a.ttot, a.G) / a.tpc);
+        const double* P = a.part3 + ((size_t)b * a.S + slot) * W;
+        s2 += P[1];
+        sbp += P[a.B + 3];
+        swa += P[a.B + 4];
+    }
+    *out = (double)a.N * a.cs.tq[c] - 2.0 * sbp + a.cs.q64[c] * s2 + swa;
+}
 
 
 // Solve the 3x3 system K x = v by Gaussian elimination with partial pivoting.
@@ -1025,7 +1111,7 @@ __global__ void __launch_bounds__(128) k2_update(UpdateArgs a) {
     extern __shared__ double sAinv[];   // [B][B] A^-1 of this column (bulk copy)
     __shared__ uint64_t abar;
     __shared__ double sh_t[128], sh_h[128];
-    __shared__ double scratch[32 * 9];
+    __shared__ double scratch[32 * 18];
     __shared__ double sh_coef[3];
     __shared__ double sh_s[3];
     __shared__ int sh_st;
@@ -1046,7 +1132,7 @@ __global__ void __launch_bounds__(128) k2_update(UpdateArgs a) {
     int b0 = (int)((c0 * a.G) / a.ttot);
     while (b0 > 0 && tile_begin(b0, a.ttot, a.G) > c0) --b0;
     while (tile_begin(b0 + 1, a.ttot, a.G) <= c0) ++b0;
-    const int W = B + 3;
+    const int W = B + kPartExtra;
     double sv = 0.0, s0 = 0.0, s2 = 0.0, ss = 0.0;
     for (int b = b0; b < a.G && tile_begin(b, a.ttot, a.G) < c1; ++b) {
         const int slot = c - (int)(tile_begin(b, a.ttot, a.G) / a.tpc);
@@ -1093,16 +1179,19 @@ __global__ void __launch_bounds__(128) k2_update(UpdateArgs a) {
             yh = fma(v, sh_h[i], yh);
         }
     }
-    // 3. G_ij = u_i . y_j, u = (t', t, h), y = (A^-1 t', A^-1 t, A^-1 h)
-    double gv[9];
+    // 3. G_ij = u_i . y_j, u = (t', t, h), y = (A^-1 t', A^-1 t, A^-1 h); YY_ij = y_i . y_j
+    double gv[18];
     {
         const double u[3] = {tp, t, h}, y[3] = {yp, yt, yh};
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-            for (int j = 0; j < 3; ++j) gv[i * 3 + j] = tid < B ? u[i] * y[j] : 0.0;
+            for (int j = 0; j < 3; ++j) {
+                gv[i * 3 + j] = tid < B ? u[i] * y[j] : 0.0;
+                gv[9 + i * 3 + j] = tid < B ? y[i] * y[j] : 0.0;
+            }
     }
-    block_sum<9>(gv, scratch);
+    block_sum<18>(gv, scratch);
     if (tid == 0) {
         // C^k = C0 + U M U^T, M in the basis (t', t, h)
         const double M[3][3] = {{bbar * bbar, -bbar * bbar, 0.0}, {-bbar * bbar, b2, -1.0}, {0.0, -1.0, 0.0}};
@@ -1123,6 +1212,7 @@ __global__ void __launch_bounds__(128) k2_update(UpdateArgs a) {
             sh_coef[i] = s;
         }
         sh_st = st;
+        cs.tq[c] = woodbury_trace(M, gv, gv + 9, B, cs.rho64[c], cs.tra[c], bbar);
     }
     __syncthreads();
     // 4. z = y_t - Y M (I + G M)^-1 U^T A^-1 t   (Woodbury)
@@ -1166,7 +1256,7 @@ struct SweepArgs {
     double* part3;         // [G][S][B+3]
     int cols, N, B, tpc, G, S;
     long long ttot;
-    int k, n_iter, use_sparsity, use_albedo;
+    int k, n_iter, use_sparsity, use_albedo, energy;
     float eps, r_floor;
 };
 
@@ -1176,7 +1266,7 @@ __global__ void __launch_bounds__(kTileRows, 2)
              SweepArgs a) {
     using Gm = SweepGeom<NQ>;
     constexpr int B4 = NQ * 4;
-    constexpr int W = B4 + 3;
+    constexpr int W = B4 + kPartExtra;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* stages = align1024(smem_raw);
     __shared__ uint64_t full[kStages];
@@ -1190,7 +1280,8 @@ __global__ void __launch_bounds__(kTileRows, 2)
     const long long tb = tile_begin(blockIdx.x, a.ttot, a.G), te = tile_begin(blockIdx.x + 1, a.ttot, a.G);
     const int ntl = (int)(te - tb);
     const int cfirst = (int)(tb / a.tpc);
-    const bool accum = a.k < a.n_iter;
+    const bool accum = a.k < a.n_iter;           // statistics for iteration k + 1
+    const bool acce = accum || a.energy;          // partials written (energy: every sweep)
 
     if (tid == 0) {
         prefetch_tmap(&tm_main);
@@ -1216,7 +1307,7 @@ __global__ void __launch_bounds__(kTileRows, 2)
     float acc[B4];
 #pragma unroll
     for (int i = 0; i < B4; ++i) acc[i] = 0.f;
-    float sb = 0.f, sb2 = 0.f, sbs = 0.f;
+    float sb = 0.f, sb2 = 0.f, sbs = 0.f, sbp = 0.f, swa = 0.f;
 
     auto flush = [&](int slot) {
         // fixed-order warp butterfly, then fp64 across warps -> part3[blockIdx][slot]
@@ -1232,6 +1323,8 @@ __global__ void __launch_bounds__(kTileRows, 2)
             sb += __shfl_xor_sync(0xffffffffu, sb, off);
             sb2 += __shfl_xor_sync(0xffffffffu, sb2, off);
             sbs += __shfl_xor_sync(0xffffffffu, sbs, off);
+            sbp += __shfl_xor_sync(0xffffffffu, sbp, off);
+            swa += __shfl_xor_sync(0xffffffffu, swa, off);
         }
         if (lane == 0) {
             red[wid][0] = sb;
@@ -1239,6 +1332,8 @@ __global__ void __launch_bounds__(kTileRows, 2)
             red[wid][2] = sbs;
 #pragma unroll
             for (int i = 0; i < B4; ++i) red[wid][3 + i] = acc[i];
+            red[wid][B4 + 3] = sbp;
+            red[wid][B4 + 4] = swa;
         }
         __syncthreads();
         if (tid < W) {
@@ -1250,7 +1345,7 @@ __global__ void __launch_bounds__(kTileRows, 2)
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < B4; ++i) acc[i] = 0.f;
-        sb = sb2 = sbs = 0.f;
+        sb = sb2 = sbs = sbp = swa = 0.f;
     };
 
     int cur = -1;
@@ -1261,7 +1356,7 @@ __global__ void __launch_bounds__(kTileRows, 2)
         const int c = ccur.c;
         const int row0 = ccur.tt * kTileRows;
         if (c != cur) {
-            if (cur >= 0 && accum) flush(cur - cfirst);
+            if (cur >= 0 && acce) flush(cur - cfirst);
             if (tid < B4) {
                 zs[tid] = a.z32[(size_t)c * a.B + tid];
                 ms[tid] = a.mhat32[(size_t)c * a.B + tid];
@@ -1330,16 +1425,26 @@ __global__ void __launch_bounds__(kTileRows, 2)
                 const float rr = a.use_albedo ? r : 1.f;
                 const float rt = a.use_albedo ? fmaxf(r, a.r_floor) : 1.f;
                 float out;
+                float w = 0.f;
                 if (a.k == 0) {
                     const float a0 = pz / (rt * q);                        // line 6
                     out = a.n_iter == 0 ? a0 : (a0 > 0.f ? a0 : 0.f);      // reading C3
                     a.alb[pix] = rr;
                 } else {
-                    const float w = a.use_sparsity ? 1.f / (aprev + a.eps) : 0.f;   // Eq. 5
-                    const float x = (pz - w) / (rt * q);                             // line 16
-                    out = x > 0.f ? x : 0.f;                                         // reading C14
+                    w = a.use_sparsity ? 1.f / (aprev + a.eps) : 0.f;      // Eq. 5
+                    const float x = (pz - w) / (rt * q);                   // line 16
+                    out = x > 0.f ? x : 0.f;                               // reading C14
                 }
                 a.enh[pix] = out;
+                if (a.energy) {
+                    const float beta = rt * out;
+                    sbp = fmaf(beta, pz, sbp);
+                    swa = fmaf(rt * w, fabsf(out), swa);
+                    if (!accum) {   // last sweep: the scalar sums only
+                        sb += beta;
+                        sb2 = fmaf(beta, beta, sb2);
+                    }
+                }
                 if (accum) {
                     const float beta = rt * out;
                     sb += beta;
@@ -1359,7 +1464,7 @@ __global__ void __launch_bounds__(kTileRows, 2)
         __syncthreads();
         if (tid == 0 && i + kStages < ntl) issue(i + kStages);
     }
-    if (cur >= 0 && accum) flush(cur - cfirst);
+    if (cur >= 0 && acce) flush(cur - cfirst);
 }
 
 // ---------------------------------------------------------------- misc

@@ -31,6 +31,7 @@ struct smf_ctx {
     double eps = 1e-2, ridge = 0.0, r_floor = 0.05;
     int n_iter = 30, use_sparsity = 1, use_albedo = 1;
     int stats_kernel = SMF_STATS_AUTO;
+    int energy = 0;   // energy trace (smf_set_energy_trace)
     int last_launches = 0;
     char err[512] = {0};
     // profiling (smf_profile_*): events bracketing each launch
@@ -122,7 +123,8 @@ struct Plan {
     size_t smem1, smem2, smem3;
     // workspace offsets
     size_t o_mbar, o_mu, o_tprev, o_yprev, o_ainv, o_q64, o_z32, o_mhat, o_kc, o_q32, o_status, o_pilot, o_ghat, o_part1,
-        o_part3, total;
+        o_part3, o_tra, o_rho, o_tq, o_energy, total;
+    int n_energy;   // energy rows (n_iter + 1) or 0
 };
 
 int sweep_blocks_per_sm(int B);
@@ -200,7 +202,12 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.o_pilot = take(cb * 4);
     p.o_ghat = take(cb * 4);
     p.o_part1 = p.wide ? take((size_t)cols * p.NGw * kWideNT1 * 64 * 8) : take((size_t)p.G1 * p.S1 * p.W1 * 8);
-    p.o_part3 = take((size_t)p.G * p.S * (B + 3) * 8);
+    p.o_part3 = take((size_t)p.G * p.S * (B + kPartExtra) * 8);
+    p.o_tra = take((size_t)cols * 8);
+    p.o_rho = take((size_t)cols * 8);
+    p.o_tq = take((size_t)cols * 8);
+    p.n_energy = ctx->energy ? ctx->n_iter + 1 : 0;
+    p.o_energy = take((size_t)std::max(p.n_energy, 1) * cols * 8);
     p.total = o;
     return true;
 }
@@ -414,6 +421,9 @@ ColState col_state(const Plan& p, unsigned char* ws, const float* s) {
     cs.q32 = (float*)(ws + p.o_q32);
     cs.status = (int*)(ws + p.o_status);
     cs.s = s;
+    cs.tra = (double*)(ws + p.o_tra);
+    cs.rho64 = (double*)(ws + p.o_rho);
+    cs.tq = (double*)(ws + p.o_tq);
     return cs;
 }
 
@@ -684,6 +694,27 @@ smf_status smf_set_iterations(smf_ctx* ctx, int n_iter, int use_sparsity, int us
     return SMF_OK;
 }
 
+smf_status smf_set_energy_trace(smf_ctx* ctx, int enable) {
+    if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    ctx->energy = enable ? 1 : 0;
+    return SMF_OK;
+}
+
+smf_status smf_energy_trace(smf_ctx* ctx, const void* workspace, int cols, int pixels, double* energy_out,
+                            void* stream) {
+    if (!ctx || !workspace || !energy_out || cols < 1 || pixels < 2) return SMF_ERR_INVALID_ARGUMENT;
+    if (!ctx->energy) {
+        set_err(ctx, "energy trace not enabled (smf_set_energy_trace)");
+        return SMF_ERR_NOT_CONFIGURED;
+    }
+    Plan p;
+    make_plan(ctx, cols, pixels, p);
+    cudaError_t e = cudaMemcpyAsync(energy_out, (const unsigned char*)workspace + p.o_energy,
+                                    (size_t)p.n_energy * cols * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "energy_trace copy");
+    return SMF_OK;
+}
+
 smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind) {
     if (!ctx || kind < SMF_STATS_AUTO || kind > SMF_STATS_TENSOR) return SMF_ERR_INVALID_ARGUMENT;
     if (kind == SMF_STATS_TENSOR && !k1tc_fits(ctx->bands)) {
@@ -754,9 +785,12 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     sa.use_albedo = ctx->use_albedo;
     sa.eps = (float)ctx->eps;
     sa.r_floor = (float)ctx->r_floor;
+    sa.energy = ctx->energy;
     UpdateArgs ua;
     ua.cs = cs;
     ua.part3 = sa.part3;
+    ua.energy = (double*)(ws + p.o_energy);
+    ua.k = 0;
     ua.cols = cols;
     ua.N = pixels;
     ua.B = p.B;
@@ -799,6 +833,13 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
         }
         if (e != cudaSuccess) return cuda_fail(ctx, e, "sweep launch");
         ++launches;
+        if (ctx->energy) {   // Eq. 8 energy of iteration k from the sweep's partials
+            ua.k = k;
+            k_energy<<<(cols + 127) / 128, 128, 0, st>>>(ua);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "k_energy launch");
+            ++launches;
+        }
     }
     if (column_status) {
         k_copy_status<<<(cols + 255) / 256, 256, 0, st>>>(cs.status, column_status, cols);

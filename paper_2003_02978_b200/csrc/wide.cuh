@@ -376,6 +376,7 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
         block_sum<1>(loc, scratch);
         if (tid == 0) {
             const double rho = a.ridge_rel * loc[0] / (double)B;
+            a.cs.rho64[c] = rho;
             double amax = 0.0;
             for (int b = 0; b < B; ++b) {
                 A[(size_t)b * B + b] += rho;
@@ -433,17 +434,25 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
         a.cs.kc32[2 * c + 1] = (float)qc[2];
         a.cs.status[c] = st;
     }
+    // tr((C0 + rho I)^-1) for the energy trace (fixed order)
+    double tl[1] = {0.0};
+    for (int b = tid; b < B; b += nt) tl[0] += A[(size_t)b * B + b];
+    block_sum<1>(tl, scratch);
+    if (tid == 0) {
+        a.cs.tra[c] = tl[0];
+        a.cs.tq[c] = (double)B - a.cs.rho64[c] * tl[0];
+    }
 }
 
 // ---------------------------------------------------------------- K2w update
-__host__ inline size_t k2w_update_smem(int B) { return (size_t)(2 * B + 32 * 9) * 8; }
+__host__ inline size_t k2w_update_smem(int B) { return (size_t)(2 * B + 32 * 18) * 8; }
 
 __global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
     extern __shared__ double w3_smem[];
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x, nt = blockDim.x;
     double* sh_t = w3_smem;        // [B]
     double* sh_h = sh_t + B;       // [B]
-    double* scratch = sh_h + B;    // [32][9]
+    double* scratch = sh_h + B;    // [32][18]
     __shared__ double sh_coef[3], sh_s[3];
     __shared__ int sh_st;
     ColState& cs = a.cs;
@@ -454,7 +463,7 @@ __global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
     int b0 = (int)((c0 * a.G) / a.ttot);
     while (b0 > 0 && tile_begin(b0, a.ttot, a.G) > c0) --b0;
     while (tile_begin(b0 + 1, a.ttot, a.G) <= c0) ++b0;
-    const int W = B + 3;
+    const int W = B + kPartExtra;
     const double invN = 1.0 / (double)a.N;
     if (tid == 0) {
         double s0 = 0.0, s2 = 0.0, ss = 0.0;
@@ -491,9 +500,9 @@ __global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
     }
     __syncthreads();
     // 2. y_t = A^-1 t, y_h = A^-1 h (A^-1 symmetric: column access, coalesced); 3. G
-    double gv[9];
+    double gv[18];   // G = U^T Y (9) and YY = Y^T Y (9)
 #pragma unroll
-    for (int i = 0; i < 9; ++i) gv[i] = 0.0;
+    for (int i = 0; i < 18; ++i) gv[i] = 0.0;
 #pragma unroll
     for (int jj = 0; jj < kWideMaxBPT2; ++jj) {
         const int j = tid + jj * nt;
@@ -522,9 +531,12 @@ __global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
 #pragma unroll
         for (int r = 0; r < 3; ++r)
 #pragma unroll
-            for (int q2 = 0; q2 < 3; ++q2) gv[r * 3 + q2] += u[r] * y[q2];
+            for (int q2 = 0; q2 < 3; ++q2) {
+                gv[r * 3 + q2] += u[r] * y[q2];
+                gv[9 + r * 3 + q2] += y[r] * y[q2];
+            }
     }
-    block_sum<9>(gv, scratch);
+    block_sum<18>(gv, scratch);
     if (tid == 0) {
         // C^k = C0 + U M U^T, M in the basis (t', t, h)
         const double M[3][3] = {{bbar * bbar, -bbar * bbar, 0.0}, {-bbar * bbar, b2, -1.0}, {0.0, -1.0, 0.0}};
@@ -545,6 +557,7 @@ __global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
             sh_coef[i] = s2;
         }
         sh_st = st;
+        cs.tq[c] = woodbury_trace(M, gv, gv + 9, B, cs.rho64[c], cs.tra[c], bbar);
     }
     __syncthreads();
     // 4. z = y_t - Y M (I + G M)^-1 U^T A^-1 t (Woodbury), q, mhat.z, mu.z
@@ -613,11 +626,12 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
     __shared__ float sh_aprev[kWideT3];
     __shared__ float sh_par[4];
     __shared__ int sh_st;
-    __shared__ double red[kWideNT3 / 32][3];
+    __shared__ double red[kWideNT3 / 32][5];
     const long long tb = tile_begin(blockIdx.x, a.ttot, a.G), te = tile_begin(blockIdx.x + 1, a.ttot, a.G);
     const int ntl = (int)(te - tb);
     const int cfirst = (int)(tb / a.tpc);
-    const bool accum = a.k < a.n_iter;
+    const bool accum = a.k < a.n_iter;    // statistics for iteration k + 1
+    const bool acce = accum || a.energy;   // partials written (energy: every sweep)
     // zero the ring once: the pads past the tile data stay zero
     for (size_t e = tid; e < kWideS3 * TF; e += kWideNT3) buf0[e] = 0.f;
     __syncthreads();
@@ -643,29 +657,29 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
     float acc[NBT];
 #pragma unroll
     for (int j = 0; j < NBT; ++j) acc[j] = 0.f;
-    float sb = 0.f, sb2 = 0.f, sbs = 0.f;
+    float sb = 0.f, sb2 = 0.f, sbs = 0.f, sbp = 0.f, swa = 0.f;
 
     auto flush = [&](int slot) {
-        double* P = a.part3 + ((size_t)blockIdx.x * a.S + slot) * (B + 3);
+        double* P = a.part3 + ((size_t)blockIdx.x * a.S + slot) * (B + kPartExtra);
 #pragma unroll
         for (int j = 0; j < NBT; ++j) {
             const int b = tid + j * kWideNT3;
             if (b < B) P[3 + b] = (double)acc[j];
             acc[j] = 0.f;
         }
-        float v3[3] = {sb, sb2, sbs};
+        float v3[5] = {sb, sb2, sbs, sbp, swa};
 #pragma unroll
-        for (int q = 0; q < 3; ++q) v3[q] = warp_sum_f(v3[q]);
+        for (int q = 0; q < 5; ++q) v3[q] = warp_sum_f(v3[q]);
         if (lane == 0)
-            for (int q = 0; q < 3; ++q) red[wid][q] = (double)v3[q];
+            for (int q = 0; q < 5; ++q) red[wid][q] = (double)v3[q];
         __syncthreads();
-        if (tid < 3) {
+        if (tid < 5) {
             double s = 0.0;
             for (int w = 0; w < kWideNT3 / 32; ++w) s += red[w][tid];
-            P[tid] = s;
+            P[tid < 3 ? tid : B + tid] = s;   // [0..2] and [B+3], [B+4]
         }
         __syncthreads();
-        sb = sb2 = sbs = 0.f;
+        sb = sb2 = sbs = sbp = swa = 0.f;
     };
 
     int cur = -1;
@@ -680,7 +694,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
         if (i + kWideS3 - 1 < ntl) load_tile(i + kWideS3 - 1);
         cp_async_commit();
         if (c != cur) {
-            if (cur >= 0 && accum) flush(cur - cfirst);
+            if (cur >= 0 && acce) flush(cur - cfirst);
             for (int b = tid; b < 32 * J; b += kWideNT3) {
                 zs[b] = b < B ? a.z32[(size_t)c * B + b] : 0.f;
                 ms[b] = b < B ? a.mhat32[(size_t)c * B + b] : 0.f;
@@ -761,17 +775,22 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
                         const float pz = dz[pb] + fmaf(sc, mz, -cz);  // (L - mu^k).z
                         const float rt = a.use_albedo ? fmaxf(r0, a.r_floor) : 1.f;
                         float out;
+                        float w = 0.f;
                         if (a.k == 0) {
                             const float a0 = pz / (rt * q);                       // line 6
                             out = a.n_iter == 0 ? a0 : (a0 > 0.f ? a0 : 0.f);     // reading C3
                             a.alb[pix] = a.use_albedo ? r0 : 1.f;
                         } else {
-                            const float w = a.use_sparsity ? 1.f / (sh_aprev[pp] + a.eps) : 0.f;   // Eq. 5
-                            const float x = (pz - w) / (rt * q);                                  // line 16
-                            out = x > 0.f ? x : 0.f;                                              // C14
+                            w = a.use_sparsity ? 1.f / (sh_aprev[pp] + a.eps) : 0.f;   // Eq. 5
+                            const float x = (pz - w) / (rt * q);                      // line 16
+                            out = x > 0.f ? x : 0.f;                                  // C14
                         }
                         a.enh[pix] = out;
                         beta = rt * out;
+                        if (a.energy) {
+                            sbp = fmaf(beta, pz, sbp);
+                            swa = fmaf(rt * w, fabsf(out), swa);
+                        }
                     }
                 }
                 sh_bs[pp] = make_float2(beta, sc);
@@ -818,7 +837,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
         }
         __syncthreads();   // slot i % S free for tile i + S
     }
-    if (cur >= 0 && accum) flush(cur - cfirst);
+    if (cur >= 0 && acce) flush(cur - cfirst);
 }
 
 }  // namespace smf

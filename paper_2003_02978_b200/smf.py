@@ -40,6 +40,8 @@ SYMBOLS = {
     "smf_initial_statistics": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp]),
     "smf_last_launch_count": (_i, [_vp]),
     "smf_set_stats_kernel": (_i, [_vp, _i]),
+    "smf_set_energy_trace": (_i, [_vp, _i]),
+    "smf_energy_trace": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "smf_stats_kernel_used": (_i, [_vp]),
     "smf_profile_enable": (_i, [_vp, _i]),
     "smf_profile_read": (_i, [_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_i)]),
@@ -81,7 +83,7 @@ class Retriever:
     STATS_KERNELS = {"auto": 0, "ffma": 1, "tensor": 2}
 
     def __init__(self, bands, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2, ridge_rel=0.0,
-                 r_floor=0.05, stats_kernel="auto"):
+                 r_floor=0.05, stats_kernel="auto", energy=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("smf needs a CUDA device (no CPU fallback)")
@@ -94,7 +96,18 @@ class Retriever:
         self._check(_lib.smf_set_regularisation(self._h, float(eps), float(ridge_rel), float(r_floor)))
         self._check(_lib.smf_set_iterations(self._h, int(n_iter), int(bool(use_sparsity)), int(bool(use_albedo))))
         self._check(_lib.smf_set_stats_kernel(self._h, self.STATS_KERNELS[stats_kernel]))
+        self._check(_lib.smf_set_energy_trace(self._h, int(bool(energy))))
         self.n_iter = int(n_iter)
+
+    def energy_trace(self, workspace, cols, pixels, stream=None):
+        """Eq. 8 energy per iteration and column (fp64 [n_iter + 1][cols]) of the last
+        retrieve that used `workspace` (requires energy=True)."""
+        import torch
+        out = torch.empty((self.n_iter + 1, cols), dtype=torch.float64, device=workspace.device)
+        st = stream if stream is not None else torch.cuda.current_stream(workspace.device)
+        self._check(_lib.smf_energy_trace(self._h, _ptr(workspace), cols, pixels, _ptr(out),
+                                          ctypes.c_void_p(st.cuda_stream)))
+        return out
 
     @property
     def stats_kernel_used(self) -> str:

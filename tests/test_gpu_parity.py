@@ -214,6 +214,35 @@ def test_stress_columns_parity(smf, torch):
     assert rep["zero_set_agreement"] > 0.999
 
 
+# ------------------------------------------------------------------ energy trace (Eq. 8, NEXT f2)
+@pytest.mark.parametrize("name,cols,kw", [
+    ("tiny", 3, dict(n_iter=10)), ("tiny", 2, dict(n_iter=6, use_sparsity=0)),
+    ("tiny", 2, dict(n_iter=5, use_albedo=0, ridge_rel=1e-3)), ("segment", 2, dict(n_iter=30)),
+    ("wide13", 2, dict(n_iter=6)), ("tiny", 2, dict(n_iter=0))])
+def test_energy_trace_vs_oracle(smf, torch, name, cols, kw):
+    """The GPU energy trace, assembled from sufficient statistics and a rank-3 Woodbury
+    trace, against the oracle's literal per-pixel Eq. 8 (reading C19). fp32 sweep sums:
+    relative bar 1e-4."""
+    if name == "wide13":
+        cfg = synth.scaled(synth.CONFIGS["tiny"], cols=cols, pixels=400, bands=13, rank=8)
+        cube, s, _ = synth.generate(cfg)
+    else:
+        cfg = synth.scaled(synth.CONFIGS[name], cols=cols)
+        cube, s, _ = synth.generate(cfg, columns=list(range(cols)))
+    r = smf.Retriever(cube.shape[2], s, energy=True, **kw)
+    rad = torch.from_numpy(np.ascontiguousarray(cube)).cuda()
+    ws = r.alloc_workspace(cube.shape[0], cube.shape[1])
+    enh, alb, st = r.retrieve(rad, workspace=ws)
+    assert r.synchronize(st) == -1
+    E = r.energy_trace(ws, cube.shape[0], cube.shape[1]).cpu().numpy()
+    okw = oracle_kw(kw)
+    for c in range(cube.shape[0]):
+        *_, dg = oracle.retrieve_column(cube[c], s, diagnostics=True, **okw)
+        rel = np.abs(E[:, c] / dg["energy"] - 1)
+        print(name, c, "energy rel err max", rel.max(), "E0", dg["energy"][0], "Elast", dg["energy"][-1])
+        assert rel.max() < 1e-4
+
+
 def test_column_status_codes(smf, torch):
     cfg = synth.scaled(synth.CONFIGS["tiny"], cols=5)
     cube, s, _ = synth.generate(cfg)
