@@ -163,6 +163,22 @@ enum { SMF_STATS_AUTO = 0, SMF_STATS_FFMA = 1, SMF_STATS_TENSOR = 2 };
 smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind);
 int smf_stats_kernel_used(const smf_ctx* ctx);
 
+/* Detector grouping (the paper processes 5 adjacent detectors per
+ * partition, and all 598 together for the convergence study):
+ * with group = G > 1, smf_retrieve pools G adjacent columns into one partition
+ * (one mean, covariance, target and albedo reference per partition, Fig. alg applied
+ * to the partition's G * pixels rows); the cols % G columns left over form a ragged
+ * remainder partition (598 = 119 x 5 + 3), and G >= cols is the all-columns mode.
+ * Layouts are unchanged ([cols][pixels][bands] in, [cols][pixels] out, column_status
+ * per column = the status of its partition); smf_workspace_bytes accounts for the
+ * grouping; smf_energy_trace then returns [N_iter + 1][partitions]. G = 1 (default)
+ * is one partition per column. smf_column_model and smf_initial_statistics
+ * always treat each column as a partition.
+ * smf_group_partitions: number of partitions and (optional, host int[n]) the first
+ * column of each. */
+smf_status smf_set_grouping(smf_ctx* ctx, int group);
+smf_status smf_group_partitions(int cols, int group, int* n_partitions, int* first_cols);
+
 /* Energy trace (the objective of Eq. 8, tracked over the iterations in
  * Fig. 4). When enabled, smf_retrieve also records per column and per
  * iteration k = 0..N_iter

@@ -1473,6 +1473,12 @@ __global__ void k_copy_status(const int* src, int32_t* dst, int n) {
     if (i < n) dst[i] = src[i];
 }
 
+// detector grouping: column c takes the status of its partition c / G
+__global__ void k_expand_status(const int32_t* part_status, int32_t* dst, int cols, int G) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < cols) dst[c] = part_status[c / G];
+}
+
 struct ModelArgs {
     const double* mu;
     const double* q64;

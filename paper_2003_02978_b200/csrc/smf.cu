@@ -32,6 +32,7 @@ struct smf_ctx {
     int n_iter = 30, use_sparsity = 1, use_albedo = 1;
     int stats_kernel = SMF_STATS_AUTO;
     int energy = 0;   // energy trace (smf_set_energy_trace)
+    int group = 1;    // detector columns per partition (smf_set_grouping)
     int last_launches = 0;
     char err[512] = {0};
     // profiling (smf_profile_*): events bracketing each launch
@@ -448,6 +449,40 @@ smf_status validate(smf_ctx* ctx, const void* rad, int cols, int pixels, const v
     return SMF_OK;
 }
 
+// Detector grouping: partitions of G adjacent columns plus a
+// ragged remainder; G >= cols is the all-detectors mode.
+struct GroupLayout {
+    int G, nfull, rem, parts;
+    size_t o_full, o_rem, o_status, total;
+    static GroupLayout make(int cols, int group) {
+        GroupLayout g;
+        g.G = group >= cols ? cols : group;
+        g.nfull = cols / g.G;
+        g.rem = cols - g.nfull * g.G;
+        g.parts = g.nfull + (g.rem > 0 ? 1 : 0);
+        g.o_full = g.o_rem = g.o_status = g.total = 0;
+        return g;
+    }
+    size_t bytes(const smf_ctx* ctx, int pixels) {
+        smf_ctx tmp = *ctx;   // plan without grouping
+        tmp.group = 1;
+        Plan pf, pr;
+        make_plan(&tmp, nfull, G * pixels, pf);
+        size_t o = 0;
+        o_full = o;
+        o = align_up(o + pf.total, 256);
+        if (rem > 0) {
+            make_plan(&tmp, 1, rem * pixels, pr);
+            o_rem = o;
+            o = align_up(o + pr.total, 256);
+        }
+        o_status = o;
+        o = align_up(o + (size_t)parts * 4, 256);
+        total = o;
+        return total;
+    }
+};
+
 // K0 pilot + K1 stats + K2 init (shared by retrieve and initial_statistics)
 smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned char* ws, cudaStream_t st,
                         double* mean_out, double* cov_out, int stats_only, int& launches) {
@@ -707,10 +742,30 @@ smf_status smf_energy_trace(smf_ctx* ctx, const void* workspace, int cols, int p
         set_err(ctx, "energy trace not enabled (smf_set_energy_trace)");
         return SMF_ERR_NOT_CONFIGURED;
     }
-    Plan p;
-    make_plan(ctx, cols, pixels, p);
-    cudaError_t e = cudaMemcpyAsync(energy_out, (const unsigned char*)workspace + p.o_energy,
-                                    (size_t)p.n_energy * cols * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+    GroupLayout g = GroupLayout::make(cols, ctx->group);
+    cudaError_t e = cudaSuccess;
+    if (g.G == 1) {
+        Plan p;
+        make_plan(ctx, cols, pixels, p);
+        e = cudaMemcpyAsync(energy_out, (const unsigned char*)workspace + p.o_energy, (size_t)p.n_energy * cols * 8,
+                            cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+    } else {
+        // [n_iter+1][partitions]: the full groups, then the remainder partition
+        g.bytes(ctx, pixels);
+        smf_ctx tmp = *ctx;
+        tmp.group = 1;
+        Plan pf;
+        make_plan(&tmp, g.nfull, g.G * pixels, pf);
+        const unsigned char* ws = (const unsigned char*)workspace;
+        e = cudaMemcpy2DAsync(energy_out, (size_t)g.parts * 8, ws + g.o_full + pf.o_energy, (size_t)g.nfull * 8,
+                              (size_t)g.nfull * 8, pf.n_energy, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+        if (e == cudaSuccess && g.rem > 0) {
+            Plan pr;
+            make_plan(&tmp, 1, g.rem * pixels, pr);
+            e = cudaMemcpy2DAsync(energy_out + g.nfull, (size_t)g.parts * 8, ws + g.o_rem + pr.o_energy, 8, 8,
+                                  pr.n_energy, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+        }
+    }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "energy_trace copy");
     return SMF_OK;
 }
@@ -730,16 +785,69 @@ int smf_stats_kernel_used(const smf_ctx* ctx) {
     return (ctx->stats_kernel != SMF_STATS_FFMA && k1tc_fits(ctx->bands)) ? SMF_STATS_TENSOR : SMF_STATS_FFMA;
 }
 
+smf_status smf_group_partitions(int cols, int group, int* n_partitions, int* first_cols) {
+    if (cols < 1 || group < 1 || !n_partitions) return SMF_ERR_INVALID_ARGUMENT;
+    const GroupLayout g = GroupLayout::make(cols, group);
+    *n_partitions = g.parts;
+    if (first_cols)
+        for (int k = 0; k < g.parts; ++k) first_cols[k] = k * g.G;
+    return SMF_OK;
+}
+
+smf_status smf_set_grouping(smf_ctx* ctx, int group) {
+    if (!ctx || group < 1) return SMF_ERR_INVALID_ARGUMENT;
+    ctx->group = group;
+    return SMF_OK;
+}
+
 smf_status smf_workspace_bytes(const smf_ctx* ctx, int cols, int pixels, size_t* bytes) {
     if (!ctx || !bytes || cols < 1 || pixels < 2) return SMF_ERR_INVALID_ARGUMENT;
-    Plan p;
-    make_plan(ctx, cols, pixels, p);
-    *bytes = p.total;
+    GroupLayout g = GroupLayout::make(cols, ctx->group);
+    if (g.G == 1) {
+        Plan p;
+        make_plan(ctx, cols, pixels, p);
+        *bytes = p.total;
+        return SMF_OK;
+    }
+    *bytes = g.bytes(ctx, pixels);
     return SMF_OK;
 }
 
 smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixels, float* enhancement,
                         float* albedo, void* workspace, int32_t* column_status, void* stream) {
+    if (ctx && ctx->group > 1 && cols >= 1) {
+        // detector grouping: the full groups are one retrieval over nfull partitions of
+        // G * pixels rows (the G columns of a group are contiguous in [cols][pixels][bands]),
+        // the ragged remainder a second one; partition status expanded to columns
+        GroupLayout g = GroupLayout::make(cols, ctx->group);
+        if (g.G > 1) {
+            if (!radiance || !workspace || !enhancement || !albedo || pixels < 2) return SMF_ERR_INVALID_ARGUMENT;
+            g.bytes(ctx, pixels);   // region offsets
+            unsigned char* ws = (unsigned char*)workspace;
+            int32_t* pst = (int32_t*)(ws + g.o_status);
+            const int saved = ctx->group;
+            ctx->group = 1;
+            smf_status rc = smf_retrieve(ctx, radiance, g.nfull, g.G * pixels, enhancement, albedo,
+                                         ws + g.o_full, pst, stream);
+            int launches = ctx->last_launches;
+            if (rc == SMF_OK && g.rem > 0) {
+                const size_t off = (size_t)g.nfull * g.G * pixels;
+                rc = smf_retrieve(ctx, radiance + off * ctx->bands, 1, g.rem * pixels, enhancement + off,
+                                  albedo + off, ws + g.o_rem, pst + g.nfull, stream);
+                launches += ctx->last_launches;
+            }
+            ctx->group = saved;
+            if (rc != SMF_OK) return rc;
+            if (column_status) {
+                k_expand_status<<<(cols + 255) / 256, 256, 0, (cudaStream_t)stream>>>(pst, column_status, cols, g.G);
+                ++launches;
+                cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) return cuda_fail(ctx, e, "expand status");
+            }
+            ctx->last_launches = launches;
+            return SMF_OK;
+        }
+    }
     smf_status v = validate(ctx, radiance, cols, pixels, workspace);
     if (v != SMF_OK) return v;
     if (!enhancement || !albedo || (void*)enhancement == (void*)albedo ||
@@ -892,8 +1000,10 @@ smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols,
         for (int k = 0; k < 6 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&ctx->h_ev[k], cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "stream create");
     }
-    const int nchunks = std::max(1, std::min(8, cols / 64));
-    const int ccols = (cols + nchunks - 1) / nchunks;   // columns per chunk (last may be short)
+    const int G = std::min(ctx->group, cols);   // chunks hold whole detector groups
+    const int ngroups = (cols + G - 1) / G;
+    const int nchunks = std::max(1, std::min(std::min(8, cols / 64), ngroups));
+    const int ccols = (ngroups + nchunks - 1) / nchunks * G;   // columns per chunk (last may be short)
     size_t ws_bytes = 0, ws_last = 0;
     smf_workspace_bytes(ctx, ccols, pixels, &ws_bytes);
     smf_workspace_bytes(ctx, cols - (nchunks - 1) * ccols > 0 ? cols - (nchunks - 1) * ccols : ccols, pixels,

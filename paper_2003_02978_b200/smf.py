@@ -41,6 +41,8 @@ SYMBOLS = {
     "smf_last_launch_count": (_i, [_vp]),
     "smf_set_stats_kernel": (_i, [_vp, _i]),
     "smf_set_energy_trace": (_i, [_vp, _i]),
+    "smf_set_grouping": (_i, [_vp, _i]),
+    "smf_group_partitions": (_i, [_i, _i, ctypes.POINTER(_i), ctypes.POINTER(_i)]),
     "smf_energy_trace": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "smf_stats_kernel_used": (_i, [_vp]),
     "smf_profile_enable": (_i, [_vp, _i]),
@@ -73,6 +75,16 @@ def supported_bands(bands: int) -> bool:
     return bool(_lib.smf_supported_bands(int(bands)))
 
 
+def group_partitions(cols: int, group: int) -> list:
+    """First column of every partition for detector grouping (smf_group_partitions)."""
+    n = _i()
+    if _lib.smf_group_partitions(int(cols), int(group), ctypes.byref(n), None) != SMF_OK:
+        raise SMFError(SMF_ERR_INVALID_ARGUMENT, "bad grouping request")
+    first = (_i * max(n.value, 1))()
+    _lib.smf_group_partitions(int(cols), int(group), ctypes.byref(n), first)
+    return list(first[: n.value])
+
+
 def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
@@ -83,7 +95,7 @@ class Retriever:
     STATS_KERNELS = {"auto": 0, "ffma": 1, "tensor": 2}
 
     def __init__(self, bands, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2, ridge_rel=0.0,
-                 r_floor=0.05, stats_kernel="auto", energy=False):
+                 r_floor=0.05, stats_kernel="auto", energy=False, group=1):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("smf needs a CUDA device (no CPU fallback)")
@@ -97,13 +109,17 @@ class Retriever:
         self._check(_lib.smf_set_iterations(self._h, int(n_iter), int(bool(use_sparsity)), int(bool(use_albedo))))
         self._check(_lib.smf_set_stats_kernel(self._h, self.STATS_KERNELS[stats_kernel]))
         self._check(_lib.smf_set_energy_trace(self._h, int(bool(energy))))
+        self._check(_lib.smf_set_grouping(self._h, int(group)))
+        self.group = int(group)
         self.n_iter = int(n_iter)
 
     def energy_trace(self, workspace, cols, pixels, stream=None):
-        """Eq. 8 energy per iteration and column (fp64 [n_iter + 1][cols]) of the last
-        retrieve that used `workspace` (requires energy=True)."""
+        """Eq. 8 energy per iteration and partition (fp64 [n_iter + 1][partitions]; one
+        partition per column unless grouped) of the last retrieve that used `workspace`
+        (requires energy=True)."""
         import torch
-        out = torch.empty((self.n_iter + 1, cols), dtype=torch.float64, device=workspace.device)
+        nparts = len(group_partitions(cols, self.group))
+        out = torch.empty((self.n_iter + 1, nparts), dtype=torch.float64, device=workspace.device)
         st = stream if stream is not None else torch.cuda.current_stream(workspace.device)
         self._check(_lib.smf_energy_trace(self._h, _ptr(workspace), cols, pixels, _ptr(out),
                                           ctypes.c_void_p(st.cuda_stream)))

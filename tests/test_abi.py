@@ -82,3 +82,15 @@ def test_missing_library_fails_loudly(tmp_path):
     code = "import paper_2003_02978_b200.smf"
     r = subprocess.run([sys.executable, "-c", code], cwd=tmp_path, capture_output=True, text=True)
     assert r.returncode != 0 and "libsmf.so not built" in r.stderr
+
+
+def test_group_partitions_layout():
+    """Detector grouping partitions: 5-detector groups over 598
+    columns leave a ragged 3-column remainder (598 = 119 x 5 + 3); G >= cols is the
+    all-detectors mode; G = 1 is one partition per column."""
+    from paper_2003_02978_b200 import smf
+    p = smf.group_partitions(598, 5)
+    assert len(p) == 120 and p[:3] == [0, 5, 10] and p[-2:] == [590, 595]
+    assert smf.group_partitions(7, 3) == [0, 3, 6]
+    assert smf.group_partitions(7, 7) == [0] and smf.group_partitions(7, 100) == [0]
+    assert smf.group_partitions(4, 1) == [0, 1, 2, 3]

@@ -243,6 +243,37 @@ def test_energy_trace_vs_oracle(smf, torch, name, cols, kw):
         assert rel.max() < 1e-4
 
 
+# ------------------------------------------------------------------ detector grouping (NEXT f1)
+@pytest.mark.parametrize("cols,group,bands", [(7, 3, 32), (5, 5, 32), (6, 100, 32), (4, 3, 13)])
+def test_grouped_retrieval_vs_oracle(smf, torch, cols, group, bands):
+    """G adjacent detector columns form one partition, the rest a ragged
+    remainder, G >= cols all columns. The oracle runs Fig. alg on each
+    partition's pooled rows (the partition is its columns' pixels, in order)."""
+    cfg = synth.scaled(synth.CONFIGS["tiny"], cols=cols, pixels=256, bands=bands, rank=8)
+    cube, s, _ = synth.generate(cfg)
+    r = smf.Retriever(bands, s, n_iter=8, group=group, energy=True)
+    rad = torch.from_numpy(np.ascontiguousarray(cube)).cuda()
+    ws = r.alloc_workspace(cols, cfg.pixels)
+    enh, alb, st = r.retrieve(rad, workspace=ws)
+    assert r.synchronize(st) == -1
+    E = r.energy_trace(ws, cols, cfg.pixels).cpu().numpy()
+    enh, alb = enh.cpu().numpy(), alb.cpu().numpy()
+    firsts = smf.group_partitions(cols, group)
+    bounds = firsts + [cols]
+    for k, (c0, c1) in enumerate(zip(bounds[:-1], bounds[1:])):
+        part = cube[c0:c1].reshape(1, (c1 - c0) * cfg.pixels, bands)
+        a_ref, r_ref, rc, dg = oracle.retrieve_column(part[0], s, n_iter=8, diagnostics=True)
+        assert rc == 0
+        rep = compare(enh[c0:c1].reshape(-1), alb[c0:c1].reshape(-1), a_ref, r_ref, f"group {c0}:{c1}")
+        print(rep)
+        assert rep["n_bad"] == 0 and rep["albedo_max_rel"] <= 1e-5
+        assert np.abs(E[:, k] / dg["energy"] - 1).max() < 1e-4
+    # the host path keeps groups inside its column chunks
+    eh, ah, sh, rc = r.retrieve_host(cube)
+    assert rc == 0
+    print(assert_parity(eh, ah, enh.astype(np.float64), alb.astype(np.float64), "grouped host"))
+
+
 def test_column_status_codes(smf, torch):
     cfg = synth.scaled(synth.CONFIGS["tiny"], cols=5)
     cube, s, _ = synth.generate(cfg)
