@@ -200,9 +200,79 @@ def workload_config(cfg, n_gpus):
             "parallelism": "replicas" if n_gpus > 1 else "single-gpu"}
 
 
+def run_campaign(args):
+    """BASELINE.json configs[4]: 4 independent flightlines (598 x 12000 x 72, plume densities
+    0 / 0.1 / 1 / 5 %) through one GPU, once with sparsity on (30 iterations) and once as the
+    classical albedo-corrected MF (sparsity off, N_iter = 0, reading C11). Device-resident
+    throughput per mode plus the host-buffer (streamed) end-to-end number; N = 1 only."""
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2003_02978_b200 import smf, synth
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
+    scenes = []
+    for j in range(4):
+        cfg = synth.CONFIGS[f"campaign{j}"]
+        cube, s, _ = synth.generate(cfg)
+        scenes.append((cfg, torch.from_numpy(cube).to(dev), s, torch.from_numpy(cube).pin_memory()))
+        del cube
+    cfg0 = scenes[0][0]
+    out = {}
+    stream = torch.cuda.current_stream(dev)
+    for mode, n_iter, sp in (("sparse_30it", 30, True), ("albedo_mf_0it", 0, False)):
+        rets = [smf.Retriever(c.bands, s, n_iter=n_iter, use_sparsity=sp) for c, _, s, _ in scenes]
+        ws = rets[0].alloc_workspace(cfg0.cols, cfg0.pixels, dev)
+        enh = torch.empty((cfg0.cols, cfg0.pixels), dtype=torch.float32, device=dev)
+        alb, st = torch.empty_like(enh), torch.empty(cfg0.cols, dtype=torch.int32, device=dev)
+
+        def step():
+            for r, (c, rad, _, _) in zip(rets, scenes):
+                r.retrieve(rad, enh, alb, ws, st, stream)
+        for _ in range(max(args.warmup, 3)):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(0) as clk:
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        pix = sum(c.cols * c.pixels for c, *_ in scenes)
+        units = pix * max(n_iter, 1)
+        # streamed from pinned host buffers (H2D + D2H inside the region)
+        h_enh = torch.empty((cfg0.cols, cfg0.pixels), dtype=torch.float32).pin_memory()
+        h_alb, h_st = torch.empty_like(h_enh).pin_memory(), torch.empty(cfg0.cols, dtype=torch.int32).pin_memory()
+        for r, (c, _, _, h) in zip(rets, scenes):   # warm-up (context buffers)
+            r.retrieve_host_ptr(h.data_ptr(), c.cols, c.pixels, h_enh.data_ptr(), h_alb.data_ptr(), h_st.data_ptr())
+        t0 = time.perf_counter()
+        for r, (c, _, _, h) in zip(rets, scenes):
+            r.retrieve_host_ptr(h.data_ptr(), c.cols, c.pixels, h_enh.data_ptr(), h_alb.data_ptr(), h_st.data_ptr())
+        dt = time.perf_counter() - t0
+        out[mode] = {"ms_per_campaign": ms, "pixel_iterations_per_s" if n_iter else "pixels_per_s": units / (ms * 1e-3),
+                     "e2e_ms": dt * 1e3, "e2e_per_s": units / dt, "clocks": clk.summary()}
+    sp = out["sparse_30it"]
+    line = {"metric": "pixel·iterations/sec (campaign 4x598x12000x72 fp32, 30 IRL1 iterations)",
+            "value": sp["pixel_iterations_per_s"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sp["ms_per_campaign"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "campaign: 4 flightlines 598x12000x72, plume density 0/0.1/1/5 %",
+                       "l2": "inputs 8.3 GB >> L2"},
+            "e2e": {"value": sp["e2e_per_s"], "unit": UNIT,
+                    "h2d_bytes_per_step": int(sum(c.cube_bytes for c, *_ in scenes)),
+                    "d2h_bytes_per_step": int(sum(c.cols * c.pixels * 8 + c.cols * 4 for c, *_ in scenes))},
+            "campaign": out, "clocks": sp["clocks"]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     from paper_2003_02978_b200 import synth
+    if args.config == "campaign":
+        return run_campaign(args)
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
