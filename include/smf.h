@@ -163,6 +163,17 @@ enum { SMF_STATS_AUTO = 0, SMF_STATS_FFMA = 1, SMF_STATS_TENSOR = 2 };
 smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind);
 int smf_stats_kernel_used(const smf_ctx* ctx);
 
+/* On-device layout conversion of a radiance cube as stored on disk (AVIRIS-NG style,
+ * SPEC S:23) into the retrieval layout [samples][lines][bands] (samples =
+ * detector columns = cols, lines = along-track pixels):
+ *   SMF_LAYOUT_BIL: in [lines][bands][samples] (band interleaved by line);
+ *   SMF_LAYOUT_BIP: in [lines][samples][bands] (band interleaved by pixel).
+ * in, out: device fp32, caller-owned, must not overlap; enqueued on `stream`.
+ * SMF_ERR_SHAPE if BIL has more than 65535 lines (grid limit). */
+enum { SMF_LAYOUT_BIL = 0, SMF_LAYOUT_BIP = 1 };
+smf_status smf_convert_layout(const float* in, int lines, int samples, int bands, int layout, float* out,
+                              void* stream);
+
 /* Detector grouping (the paper processes 5 adjacent detectors per
  * partition, and all 598 together for the convergence study):
  * with group = G > 1, smf_retrieve pools G adjacent columns into one partition

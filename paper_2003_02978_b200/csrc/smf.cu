@@ -785,6 +785,23 @@ int smf_stats_kernel_used(const smf_ctx* ctx) {
     return (ctx->stats_kernel != SMF_STATS_FFMA && k1tc_fits(ctx->bands)) ? SMF_STATS_TENSOR : SMF_STATS_FFMA;
 }
 
+smf_status smf_convert_layout(const float* in, int lines, int samples, int bands, int layout, float* out,
+                              void* stream) {
+    if (!in || !out || (const void*)in == (const void*)out || lines < 1 || samples < 1 || bands < 1 ||
+        (layout != SMF_LAYOUT_BIL && layout != SMF_LAYOUT_BIP))
+        return SMF_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (layout == SMF_LAYOUT_BIP) {
+        const int warps = 8, gx = std::min((samples + warps - 1) / warps, 64);
+        k_bip_to_cpb<<<dim3(gx, lines), warps * 32, 0, st>>>(in, out, lines, samples, bands);
+    } else {
+        if (lines > 65535) return SMF_ERR_SHAPE;
+        k_bil_to_cpb<<<dim3((samples + 31) / 32, (bands + 31) / 32, lines), dim3(32, 8), 0, st>>>(in, out, lines,
+                                                                                                samples, bands);
+    }
+    return cudaGetLastError() == cudaSuccess ? SMF_OK : SMF_ERR_CUDA;
+}
+
 smf_status smf_group_partitions(int cols, int group, int* n_partitions, int* first_cols) {
     if (cols < 1 || group < 1 || !n_partitions) return SMF_ERR_INVALID_ARGUMENT;
     const GroupLayout g = GroupLayout::make(cols, group);

@@ -42,6 +42,7 @@ SYMBOLS = {
     "smf_set_stats_kernel": (_i, [_vp, _i]),
     "smf_set_energy_trace": (_i, [_vp, _i]),
     "smf_set_grouping": (_i, [_vp, _i]),
+    "smf_convert_layout": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
     "smf_group_partitions": (_i, [_i, _i, ctypes.POINTER(_i), ctypes.POINTER(_i)]),
     "smf_energy_trace": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "smf_stats_kernel_used": (_i, [_vp]),
@@ -73,6 +74,25 @@ def abi_version() -> int:
 
 def supported_bands(bands: int) -> bool:
     return bool(_lib.smf_supported_bands(int(bands)))
+
+
+LAYOUTS = {"BIL": 0, "BIP": 1}
+
+
+def convert_layout(cube, layout, out=None, stream=None):
+    """Device cube as stored on disk -> retrieval layout [samples][lines][bands]:
+    BIL [lines][bands][samples] or BIP [lines][samples][bands] (smf_convert_layout)."""
+    import torch
+    lines = cube.shape[0]
+    samples, bands = (cube.shape[2], cube.shape[1]) if layout == "BIL" else (cube.shape[1], cube.shape[2])
+    if out is None:
+        out = torch.empty((samples, lines, bands), dtype=torch.float32, device=cube.device)
+    st = stream if stream is not None else torch.cuda.current_stream(cube.device)
+    rc = _lib.smf_convert_layout(_ptr(cube), lines, samples, bands, LAYOUTS[layout], _ptr(out),
+                                 ctypes.c_void_p(st.cuda_stream))
+    if rc != SMF_OK:
+        raise SMFError(rc, "convert_layout")
+    return out
 
 
 def group_partitions(cols: int, group: int) -> list:

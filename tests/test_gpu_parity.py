@@ -274,6 +274,17 @@ def test_grouped_retrieval_vs_oracle(smf, torch, cols, group, bands):
     print(assert_parity(eh, ah, enh.astype(np.float64), alb.astype(np.float64), "grouped host"))
 
 
+@pytest.mark.parametrize("layout", ["BIL", "BIP"])
+def test_layout_conversion(smf, torch, layout):
+    """On-disk BIL / BIP cubes -> [samples][lines][bands] on the device: exact copy."""
+    rng = np.random.default_rng(5)
+    lines, samples, bands = 37, 70, 45
+    cpb = rng.standard_normal((samples, lines, bands)).astype(np.float32)
+    disk = cpb.transpose(1, 2, 0) if layout == "BIL" else cpb.transpose(1, 0, 2)
+    out = smf.convert_layout(torch.from_numpy(np.ascontiguousarray(disk)).cuda(), layout).cpu().numpy()
+    np.testing.assert_array_equal(out, cpb)
+
+
 def test_column_status_codes(smf, torch):
     cfg = synth.scaled(synth.CONFIGS["tiny"], cols=5)
     cube, s, _ = synth.generate(cfg)
