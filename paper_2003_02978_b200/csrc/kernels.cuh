@@ -1000,6 +1000,7 @@ struct UpdateArgs {
     const double* part3;   // [G][S][B+5]
     double* energy;        // k_energy: [n_iter+1][cols]
     int cols, N, B, tpc, G, S, k;
+    int energy_on;         // compute T_k (energy trace) in the update
     long long ttot;
 };
 
@@ -1191,7 +1192,10 @@ __global__ void __launch_bounds__(128) k2_update(UpdateArgs a) {
                 gv[9 + i * 3 + j] = tid < B ? y[i] * y[j] : 0.0;
             }
     }
-    block_sum<18>(gv, scratch);
+    if (a.energy_on)
+        block_sum<18>(gv, scratch);
+    else
+        block_sum<9>(*reinterpret_cast<double(*)[9]>(gv), scratch);
     if (tid == 0) {
         // C^k = C0 + U M U^T, M in the basis (t', t, h)
         const double M[3][3] = {{bbar * bbar, -bbar * bbar, 0.0}, {-bbar * bbar, b2, -1.0}, {0.0, -1.0, 0.0}};
@@ -1212,7 +1216,7 @@ __global__ void __launch_bounds__(128) k2_update(UpdateArgs a) {
             sh_coef[i] = s;
         }
         sh_st = st;
-        cs.tq[c] = woodbury_trace(M, gv, gv + 9, B, cs.rho64[c], cs.tra[c], bbar);
+        if (a.energy_on) cs.tq[c] = woodbury_trace(M, gv, gv + 9, B, cs.rho64[c], cs.tra[c], bbar);
     }
     __syncthreads();
     // 4. z = y_t - Y M (I + G M)^-1 U^T A^-1 t   (Woodbury)

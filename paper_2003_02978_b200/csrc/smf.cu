@@ -118,8 +118,9 @@ struct Plan {
     int G1, S1, W1, T1, tpc1, NT1, be_full;
     bool k1tc;
     // wide path (any B): K1w block grid, K3w tiles of kWideT3 pixels
-    bool wide;
-    int BEw, NBw, NGw;
+    bool wide, widetc;
+    int BEw, NBw, NGw, NBLKw;
+    size_t o_sigma;
     long long ttot1;
     size_t smem1, smem2, smem3;
     // workspace offsets
@@ -159,6 +160,8 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.BEw = (B + 2 + 7) / 8 * 8;
     p.NBw = (p.BEw / 8) * (p.BEw / 8 + 1) / 2;
     p.NGw = (p.NBw + kWideNT1 - 1) / kWideNT1;
+    p.NBLKw = (B + 2 + 127) / 128;
+    p.widetc = p.wide && ctx->stats_kernel != SMF_STATS_FFMA;
     p.k1tc = !p.wide && ctx->stats_kernel != SMF_STATS_FFMA && k1tc_fits(B);
     p.T1 = p.k1tc ? kTileTC : k1_rows(B);
     p.NT1 = p.k1tc ? K1TC<1>::NT : stats_threads(B);
@@ -173,7 +176,7 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     }
     p.W1 = p.k1tc ? p.be_full * p.be_full : k1_width_host(B);
     if (p.wide) {
-        p.smem1 = k1w_smem(B, p.BEw);
+        p.smem1 = p.widetc ? k1w_tc_smem() : k1w_smem(B, p.BEw);
         p.smem2 = k2w_init_smem(B);
         p.smem3 = k3w_smem(B);
     } else {
@@ -202,7 +205,10 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.o_status = take((size_t)cols * 4);
     p.o_pilot = take(cb * 4);
     p.o_ghat = take(cb * 4);
-    p.o_part1 = p.wide ? take((size_t)cols * p.NGw * kWideNT1 * 64 * 8) : take((size_t)p.G1 * p.S1 * p.W1 * 8);
+    const size_t bep = (size_t)p.NBLKw * 128;
+    p.o_part1 = p.wide ? take(p.widetc ? (size_t)cols * bep * bep * 8 : (size_t)cols * p.NGw * kWideNT1 * 64 * 8)
+                       : take((size_t)p.G1 * p.S1 * p.W1 * 8);
+    p.o_sigma = take(p.widetc ? (size_t)cols * N * 4 : 0);
     p.o_part3 = take((size_t)p.G * p.S * (B + kPartExtra) * 8);
     p.o_tra = take((size_t)cols * 8);
     p.o_rho = take((size_t)cols * 8);
@@ -508,6 +514,36 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k0_pilot launch");
     ++launches;
+    if (p.wide && p.widetc) {
+        float* sigma = (float*)(ws + p.o_sigma);
+        {
+            ProfScope ps(ctx, st, SMF_KERNEL_STATS);
+            const long long warps = (long long)p.cols * p.N;
+            k1w_sigma<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(rad, pa.ghat32, sigma, p.cols, p.N, p.B);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_sigma launch");
+        ++launches;
+        WideTCArgs ta;
+        ta.L = rad;
+        ta.pil32 = pa.pil32;
+        ta.ghat32 = pa.ghat32;
+        ta.sigma = sigma;
+        ta.part = (double*)(ws + p.o_part1);
+        ta.cols = p.cols;
+        ta.N = p.N;
+        ta.B = p.B;
+        ta.NBLK = p.NBLKw;
+        e = cudaFuncSetAttribute(k1w_stats_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats_tc smem attribute");
+        {
+            ProfScope ps(ctx, st, SMF_KERNEL_STATS);
+            k1w_stats_tc<<<dim3(p.NBLKw * (p.NBLKw + 1) / 2, p.cols), kTW, p.smem1, st>>>(ta);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats_tc launch");
+        ++launches;
+    }
     if (p.wide) {
         WideStatsArgs wa;
         wa.L = rad;
@@ -520,19 +556,22 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         wa.BE = p.BEw;
         wa.NB = p.NBw;
         wa.NG = p.NGw;
-        e = cudaFuncSetAttribute(k1w_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats smem attribute");
-        {
-            ProfScope ps(ctx, st, SMF_KERNEL_STATS);
-            k1w_stats<<<dim3(p.NGw, p.cols), kWideNT1, p.smem1, st>>>(wa);
+        if (!p.widetc) {
+            e = cudaFuncSetAttribute(k1w_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats smem attribute");
+            {
+                ProfScope ps(ctx, st, SMF_KERNEL_STATS);
+                k1w_stats<<<dim3(p.NGw, p.cols), kWideNT1, p.smem1, st>>>(wa);
+            }
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats launch");
+            ++launches;
         }
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats launch");
-        ++launches;
         WideInitArgs ia;
         ia.cs = col_state(p, ws, ctx->s_dev);
         ia.pil32 = pa.pil32;
         ia.part = wa.part;
+        ia.BEp = p.widetc ? p.NBLKw * 128 : 0;
         ia.mean_out = mean_out;
         ia.cov_out = cov_out;
         ia.cols = p.cols;
@@ -772,7 +811,7 @@ smf_status smf_energy_trace(smf_ctx* ctx, const void* workspace, int cols, int p
 
 smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind) {
     if (!ctx || kind < SMF_STATS_AUTO || kind > SMF_STATS_TENSOR) return SMF_ERR_INVALID_ARGUMENT;
-    if (kind == SMF_STATS_TENSOR && !k1tc_fits(ctx->bands)) {
+    if (kind == SMF_STATS_TENSOR && narrow(ctx->bands) && !k1tc_fits(ctx->bands)) {
         set_err(ctx, "tensor-core statistics kernel unavailable for %d bands", ctx->bands);
         return SMF_ERR_SHAPE;
     }
@@ -782,7 +821,8 @@ smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind) {
 
 int smf_stats_kernel_used(const smf_ctx* ctx) {
     if (!ctx) return -1;
-    return (ctx->stats_kernel != SMF_STATS_FFMA && k1tc_fits(ctx->bands)) ? SMF_STATS_TENSOR : SMF_STATS_FFMA;
+    const bool tc = narrow(ctx->bands) ? k1tc_fits(ctx->bands) : true;
+    return (ctx->stats_kernel != SMF_STATS_FFMA && tc) ? SMF_STATS_TENSOR : SMF_STATS_FFMA;
 }
 
 smf_status smf_convert_layout(const float* in, int lines, int samples, int bands, int layout, float* out,
@@ -916,6 +956,7 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     ua.part3 = sa.part3;
     ua.energy = (double*)(ws + p.o_energy);
     ua.k = 0;
+    ua.energy_on = ctx->energy;
     ua.cols = cols;
     ua.N = pixels;
     ua.B = p.B;

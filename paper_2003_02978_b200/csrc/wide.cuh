@@ -206,7 +206,8 @@ constexpr int kGJ = 32;          // Gauss-Jordan block size
 struct WideInitArgs {
     ColState cs;
     const float* pil32;
-    const double* part;    // K1w blocks [cols][NG*128][64]
+    const double* part;    // K1w blocks [cols][NG*128][64], or (BEp > 0) k1w_stats_tc [cols][BEp][BEp]
+    int BEp;
     double* mean_out;      // optional [cols][B]
     double* cov_out;       // optional [cols][B][B]
     int cols, N, B, BE, NG, use_albedo, stats_only;
@@ -334,16 +335,29 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     __shared__ int bad;
     __shared__ double sh_tol, sh_mm;
     const double invN = 1.0 / (double)a.N;
-    const double* S = a.part + (size_t)c * a.NG * kWideNT1 * 64;
+    const int BEp = a.BEp;
+    const double* S = BEp > 0 ? a.part + (size_t)c * BEp * BEp : a.part + (size_t)c * a.NG * kWideNT1 * 64;
+    // entry (i, k) of the extended-row second moments: FFMA 8x8 blocks, or the tensor-core
+    // block-pair matrix (diagonal 128-blocks symmetrised, (P + P^T)/2; lower blocks as is)
+    auto ext = [&](int i, int k) -> double {
+        if (BEp == 0) return ext_entry(S, i, k, 0);
+        if (i < k) {
+            const int t = i;
+            i = k;
+            k = t;
+        }
+        if ((i >> 7) == (k >> 7)) return 0.5 * (S[(size_t)i * BEp + k] + S[(size_t)k * BEp + i]);
+        return S[(size_t)i * BEp + k];
+    };
     double* A = a.cs.ainv + (size_t)c * B * B;
     if (tid == 0) bad = COL_OK;
     __syncthreads();
-    const double Sr = ext_entry(S, B + 1, B, 0), Srr = ext_entry(S, B, B, 0);
+    const double Sr = ext(B + 1, B), Srr = ext(B, B);
     int nonfinite = 0;
     for (int b = tid; b < B; b += nt) {
         cv[b] = (double)a.pil32[(size_t)c * B + b];
-        srx[b] = ext_entry(S, B, b, 0);
-        dm[b] = (ext_entry(S, B + 1, b, 0) + Sr * cv[b]) * invN;
+        srx[b] = ext(B, b);
+        dm[b] = (ext(B + 1, b) + Sr * cv[b]) * invN;
         if (!isfinite(dm[b])) nonfinite = 1;
     }
     __syncthreads();
@@ -351,7 +365,7 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     for (size_t e = tid; e < (size_t)B * B; e += nt) {
         const int i = (int)(e / B), k = (int)(e % B);
         if (i < k) continue;
-        const double s2 = ext_entry(S, i, k, 0) + srx[i] * cv[k] + cv[i] * srx[k] + Srr * cv[i] * cv[k];
+        const double s2 = ext(i, k) + srx[i] * cv[k] + cv[i] * srx[k] + Srr * cv[i] * cv[k];
         const double v = s2 * invN - dm[i] * dm[k];
         if (!isfinite(v)) nonfinite = 1;
         A[(size_t)i * B + k] = v;
@@ -536,7 +550,10 @@ __global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
                 gv[9 + r * 3 + q2] += y[r] * y[q2];
             }
     }
-    block_sum<18>(gv, scratch);
+    if (a.energy_on)
+        block_sum<18>(gv, scratch);
+    else
+        block_sum<9>(*reinterpret_cast<double(*)[9]>(gv), scratch);
     if (tid == 0) {
         // C^k = C0 + U M U^T, M in the basis (t', t, h)
         const double M[3][3] = {{bbar * bbar, -bbar * bbar, 0.0}, {-bbar * bbar, b2, -1.0}, {0.0, -1.0, 0.0}};
@@ -557,7 +574,7 @@ __global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
             sh_coef[i] = s2;
         }
         sh_st = st;
-        cs.tq[c] = woodbury_trace(M, gv, gv + 9, B, cs.rho64[c], cs.tra[c], bbar);
+        if (a.energy_on) cs.tq[c] = woodbury_trace(M, gv, gv + 9, B, cs.rho64[c], cs.tra[c], bbar);
     }
     __syncthreads();
     // 4. z = y_t - Y M (I + G M)^-1 U^T A^-1 t (Woodbury), q, mhat.z, mu.z
@@ -840,4 +857,219 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
     if (cur >= 0 && acce) flush(cur - cfirst);
 }
 
+}  // namespace smf
+
+namespace smf {
+// ---------------------------------------------------------------- K1w on tensor cores
+// The wide extended-row SYRK as tcgen05 kind::tf32 MMAs over 128 x 128 band blocks of
+// the extended row (BE padded to NBLK * 128). CTA (pair, column) owns one lower block
+// pair (m >= n) of one column and streams the column's pixels in 32-pixel K-blocks:
+// 8 transform warps, one per band row of the pair's two blocks (thread b loads L[p][b]
+// for the K-block's 32 pixels -- coalesced across the warp -- forms x = L - sigma_p c,
+// rho = sigma - 1, 1, splits h = RN-tf32(x), l = x - h and writes both K-major
+// SWIZZLE_128B rows with STS.128); one MMA thread; 4 epilogue warps (TMEM lanes).
+// Off-diagonal pairs accumulate S_mn = h_m h_n^T + h_m l_n^T + l_m h_n^T (two MMAs per
+// K-step), diagonal pairs P = h_m h_m^T + 2 h_m l_m^T (one MMA, symmetrised by k2w_init),
+// i.e. the split of reading C21. fp32 TMEM runs of kRunW K-blocks are folded by the
+// epilogue into the column's fp64 partial matrix [BEp][BEp] in global memory (L2).
+// sigma_p = L_p . ghat comes from k1w_sigma (one pass, fp32, the same product order as
+// the FFMA kernels use for their own transform).
+constexpr int kRunW = 8;          // K-blocks (32 px each) per fp32 TMEM run
+constexpr int kTW = 13 * 32;      // threads: 8 transform + 4 epilogue + 1 MMA warps
+
+struct WideTCArgs {
+    const float* L;
+    const float* pil32;
+    const float* ghat32;
+    const float* sigma;   // [cols][N]
+    double* part;         // [cols][BEp][BEp]
+    int cols, N, B, NBLK;
+};
+
+__global__ void k1w_sigma(const float* __restrict__ L, const float* __restrict__ ghat32, float* __restrict__ sigma,
+                          int cols, int N, int B) {
+    // a warp per pixel: lanes stride the bands, fixed-order butterfly
+    const int lane = threadIdx.x & 31;
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (gw >= (long long)cols * N) return;
+    const int c = (int)(gw / N);
+    const float* Lp = L + (size_t)gw * B;
+    const float* g = ghat32 + (size_t)c * B;
+    float s = 0.f;
+    for (int b = lane; b < B; b += 32) s = fmaf(__ldg(Lp + b), __ldg(g + b), s);
+    s = warp_sum_f(s);
+    if (lane == 0) sigma[gw] = s;
+}
+
+__host__ inline size_t k1w_tc_smem() { return 2 * (size_t)512 * 128 + 1024; }   // 2 stages x 512 rows x 128 B
+
+__global__ void __launch_bounds__(kTW, 1) k1w_stats_tc(WideTCArgs a) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* ops = align1024(smem_raw);   // [2][512 rows][128 B]
+    constexpr int STAGE = 512 * 128;
+    __shared__ uint64_t op_full[2], op_empty[2], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_sh;
+    const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    // pair index -> (m, n), m >= n (row-major lower triangle of the block grid)
+    int m = 0, n = blockIdx.x;
+    while (n > m) {
+        n -= m + 1;
+        ++m;
+    }
+    const bool diag = m == n;
+    const int c = blockIdx.y, B = a.B, N = a.N;
+    const int BEp = a.NBLK * 128;
+    const int nkb = (N + 31) / 32;
+    const uint32_t idesc256 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t idesc128 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+    for (int i = tid; i < 2 * STAGE / 16; i += kTW) reinterpret_cast<float4*>(ops)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid == 0) {
+        for (int s2 = 0; s2 < 2; ++s2) {
+            mbar_init(&op_full[s2], 8);
+            mbar_init(&op_empty[s2], 1);
+            mbar_init(&acc_full[s2], 1);
+            mbar_init(&acc_empty[s2], 4);
+        }
+        fence_mbar_init();
+    }
+    if (wid == 12) tmem_alloc(&tmem_sh, 512);
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_sh;
+
+    if (wid < 8) {
+        // ===================== transform: thread = one band row of the pair =====================
+        // threads 0..127: block m (H_m rows 0..127, L_m rows 128..255);
+        // threads 128..255: block n (H_n rows 256..383, L_n rows 384..511), idle on the diagonal
+        const int half = tid >> 7, r = tid & 127;
+        const int blk = half ? n : m;
+        const int b = blk * 128 + r;                 // extended-row index
+        const bool work = !(diag && half);
+        const float cb = b < B ? a.pil32[(size_t)c * B + b] : 0.f;
+        const float* Lc = a.L + (size_t)c * N * B;
+        const float* sg = a.sigma + (size_t)c * N;
+        const uint32_t ops0 = smem_u32(ops);
+        const uint32_t rowH = (uint32_t)(half ? 256 + r : r) * 128, rowL = rowH + 128 * 128;
+        const uint32_t sw = (uint32_t)(r & 7);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s2 = kb & 1;
+            if (kb >= 2) mbar_wait(&op_empty[s2], ((kb >> 1) - 1) & 1);
+            if (work) {
+                const int p0 = kb * 32;
+                // all 64 loads issued before any use (clamped addresses, no branches), then
+                // the extended-row entry selected per band kind
+                float lv[32], sv[32];
+                const int bl = b < B ? b : B - 1;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int p = min(p0 + j, N - 1);
+                    lv[j] = __ldg(Lc + (size_t)p * B + bl);
+                    sv[j] = __ldg(sg + p);
+                }
+                float x[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float xb = fmaf(-sv[j], cb, lv[j]);
+                    const float v = b < B ? xb : (b == B ? sv[j] - 1.f : (b == B + 1 ? 1.f : 0.f));
+                    x[j] = p0 + j < N ? v : 0.f;
+                }
+                const uint32_t base = ops0 + s2 * STAGE;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    float4 h, l;
+                    h.x = tf32_rna(x[4 * q + 0]);
+                    h.y = tf32_rna(x[4 * q + 1]);
+                    h.z = tf32_rna(x[4 * q + 2]);
+                    h.w = tf32_rna(x[4 * q + 3]);
+                    l.x = x[4 * q + 0] - h.x;
+                    l.y = x[4 * q + 1] - h.y;
+                    l.z = x[4 * q + 2] - h.z;
+                    l.w = x[4 * q + 3] - h.w;
+                    const uint32_t off = (((uint32_t)q ^ sw) << 4);
+                    sts4(base + rowH + off, h);
+                    sts4(base + rowL + off, l);
+                }
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&op_full[s2]);
+        }
+    } else if (wid < 12) {
+        // ===================== epilogue: TMEM -> fp64 partial (global) =====================
+        const int e = wid - 8, row = 32 * e + lane;      // D row = band of block m
+        double* prow = a.part + ((size_t)c * BEp + m * 128 + row) * BEp + n * 128;
+        int g = 0, run = 0;
+        bool first = true;
+        for (int kb = 0; kb < nkb; ++kb) {
+            ++run;
+            if (kb != nkb - 1 && run < kRunW) continue;
+            run = 0;
+            const int ab = g & 1;
+            mbar_wait(&acc_full[ab], (g >> 1) & 1);
+            tc_fence_after();
+            const uint32_t t0 = tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)(ab * 256);
+#pragma unroll 1
+            for (int n0 = 0; n0 < 128; n0 += 16) {
+                float v[16], u[16];
+                tmem_ld16x2(t0 + n0, t0 + 128 + n0, v, u);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const double s = (double)v[j] + (diag ? 2.0 : 1.0) * (double)u[j];
+                    prow[n0 + j] = first ? s : prow[n0 + j] + s;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            ++g;
+            first = false;
+        }
+    } else {
+        // ===================== MMA issuer =====================
+        if (lane == 0) {
+            const uint32_t ops0 = smem_u32(ops);
+            int g = 0, run = 0;
+            bool fresh = true;
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s2 = kb & 1, ab = g & 1;
+                if (fresh && g >= 2) mbar_wait(&acc_empty[ab], ((g >> 1) - 1) & 1);
+                mbar_wait(&op_full[s2], (kb >> 1) & 1);
+                tc_fence_after();
+                const uint32_t sb = ops0 + s2 * STAGE;
+                const uint32_t d = tmem + (uint32_t)(ab * 256);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const uint32_t ko = ks * 32;
+                    const uint64_t dHm = umma_desc(sb + ko, 16, 1024, 2);                   // rows 0..127
+                    const uint64_t dLm = umma_desc(sb + 128 * 128 + ko, 16, 1024, 2);       // rows 128..255
+                    const uint64_t dHn = umma_desc(sb + 256 * 128 + ko, 16, 1024, 2);       // rows 256..511
+                    const uint32_t acc0 = (fresh && ks == 0) ? 0u : 1u;
+                    if (diag) {
+                        mma_tf32(d, dHm, dHm, idesc256, acc0);                 // [h h^T | h l^T]
+                    } else {
+                        mma_tf32(d, dHm, dHn, idesc256, acc0);                 // [h_m h_n^T | h_m l_n^T]
+                        mma_tf32(d, dLm, dHn, idesc128, 1u);                   // += l_m h_n^T
+                    }
+                }
+                fresh = false;
+                mma_commit(&op_empty[s2]);
+                if (kb == nkb - 1 || ++run == kRunW) {
+                    mma_commit(&acc_full[ab]);
+                    ++g;
+                    run = 0;
+                    fresh = true;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (wid == 12) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
 }  // namespace smf

@@ -187,10 +187,14 @@ def test_wide_bands(smf, torch, cols, pixels, bands):
     print(assert_parity(enh, alb, a_ref, r_ref, f"wide {cols}x{pixels}x{bands}"))
 
 
-def test_wide_initial_statistics(smf, torch):
+@pytest.mark.parametrize("kernel", ["tensor", "ffma"])
+def test_wide_initial_statistics(smf, torch, kernel):
+    """Stress-shaped columns (B = 425): the wide statistics kernels (tensor-core block
+    pairs, reading C21; FFMA blocks) against the oracle's mu0 and C0."""
     cfg = synth.scaled(synth.CONFIGS["stress"], cols=2)
     cube, s, _ = synth.generate(cfg, columns=[0, 1])
-    r = smf.Retriever(cfg.bands, s)
+    r = smf.Retriever(cfg.bands, s, stats_kernel=kernel)
+    assert r.stats_kernel_used == kernel
     mean, cov = r.initial_statistics(torch.from_numpy(cube).cuda())
     mean, cov = mean.cpu().numpy(), cov.cpu().numpy()
     for c in range(2):
