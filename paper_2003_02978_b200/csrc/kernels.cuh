@@ -802,7 +802,7 @@ __host__ inline int k1_width_host(int B) {
 }
 
 __host__ inline size_t k2_init_smem(int B, int W1) {
-    return (size_t)B * B * 8 + (size_t)W1 * 8 + 6 * (size_t)B * 8 + 32 * 4 * 8;
+    return (size_t)B * B * 8 + (size_t)W1 * 8 + (4 * (size_t)B + 2 * 192) * 8 + 32 * 4 * 8;
 }
 
 // entry (i, k) of the extended-row second-moment sums: be > 0 -> symmetrised full
@@ -818,6 +818,10 @@ __device__ __forceinline__ double ext_entry(const double* S, int i, int k, int b
     return S[(R * (R + 1) / 2 + C) * 64 + (i & 7) * 8 + (k & 7)];
 }
 
+constexpr int kMaxSlots1 = 256;   // >= the statistics grid (one CTA per SM)
+
+// MR = ceil(B / 8): row groups of the register-resident Gauss-Jordan tile
+template <int MR>
 __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     extern __shared__ double sm2[];
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x;
@@ -826,26 +830,42 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     double* dm = S + a.W1;         // [B] mean of L - c, later mu0
     double* srx = dm + B;          // [B] sum rho x
     double* cv = srx + B;          // [B] pilot c
-    double* rowj = cv + B;         // [B]
-    double* colj = rowj + B;       // [B]
-    double* vt = colj + B;         // [B] t0
+    double* rowj = cv + B;         // [2][96] pivot row (double-buffered), later mhat
+    double* colj = rowj + 192;     // [2][96] pivot column
+    double* vt = colj + 192;       // [B] t0
     double* scratch = vt + B;      // [32][4]
     __shared__ int bad;
     __shared__ double sh_tol, sh_mm;
     const double invN = 1.0 / (double)a.N;
-    // gather the K1 slots covering this column, fixed CTA order
+    // gather the K1 slots covering this column, fixed CTA order: the slot list once
+    // (thread 0), then independent loads per entry summed in that order
     {
-        const long long c0 = (long long)c * a.tpc, c1 = c0 + a.tpc;
-        int b0 = (int)((c0 * a.G1) / a.ttot);
-        while (b0 > 0 && tile_begin(b0, a.ttot, a.G1) > c0) --b0;
-        while (tile_begin(b0 + 1, a.ttot, a.G1) <= c0) ++b0;
-        for (int i = tid; i < a.W1; i += blockDim.x) {
-            double v = 0.0;
-            for (int b = b0; b < a.G1 && tile_begin(b, a.ttot, a.G1) < c1; ++b) {
+        __shared__ long long sh_slot[kMaxSlots1];   // a column spans at most G1 <= #SMs CTAs
+        __shared__ int sh_nslot;
+        if (tid == 0) {
+            const long long c0 = (long long)c * a.tpc, c1 = c0 + a.tpc;
+            int b0 = (int)((c0 * a.G1) / a.ttot);
+            while (b0 > 0 && tile_begin(b0, a.ttot, a.G1) > c0) --b0;
+            while (tile_begin(b0 + 1, a.ttot, a.G1) <= c0) ++b0;
+            int ns = 0;
+            for (int b = b0; b < a.G1 && tile_begin(b, a.ttot, a.G1) < c1 && ns < kMaxSlots1; ++b) {
                 const int slot = c - (int)(tile_begin(b, a.ttot, a.G1) / a.tpc);
-                v += a.part1[((size_t)b * a.S1 + slot) * a.W1 + i];
+                sh_slot[ns++] = ((long long)b * a.S1 + slot) * a.W1;
             }
-            S[i] = v;
+            sh_nslot = ns;
+        }
+        __syncthreads();
+        const int ns = sh_nslot;
+        for (int i = tid; i < a.W1; i += blockDim.x) {
+            double t = 0.0;
+            for (int q0 = 0; q0 < ns; q0 += 8) {   // 8 independent loads, summed in slot order
+                double v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = q0 + q < ns ? a.part1[sh_slot[q0 + q] + i] : 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) t += v[q];
+            }
+            S[i] = t;
         }
     }
     if (tid == 0) bad = COL_OK;
@@ -918,34 +938,78 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     __syncthreads();
     // in-place Gauss-Jordan inverse of the SPD matrix A = C0 + rho I (no pivoting;
     // pivot j equals the j-th Cholesky pivot squared, checked like the oracle's).
-    // Thread (ty, tx) = (tid / 32, tid % 32) owns rows ty + 8m, columns tx + 32n.
-    const int tx = tid & 31, ty = tid >> 5;
-    for (int j = 0; j < B && bad == COL_OK; ++j) {
-        for (int k = tid; k < B; k += blockDim.x) {
-            rowj[k] = A[j * B + k];
-            colj[k] = A[k * B + j];
-        }
-        __syncthreads();
-        const double piv = rowj[j];
-        if (!(piv > sh_tol) || !isfinite(piv)) {
-            if (tid == 0) bad = COL_NOT_SPD;
+    // The matrix lives in registers for the whole elimination: thread (ty, tx) =
+    // (tid / 32, tid % 32) owns rows ty + 8m (m < 12), columns tx + 32n (n < 3) (B <= 96);
+    // per pivot the owners of row / column j publish them to shared memory (double-
+    // buffered, so one barrier per pivot) and every thread updates its elements.
+    {
+        const int tx = tid & 31, ty = tid >> 5;
+        double r[MR][3];
+#pragma unroll
+        for (int m = 0; m < MR; ++m)
+#pragma unroll
+            for (int n = 0; n < 3; ++n) {
+                const int i = ty + 8 * m, k = tx + 32 * n;
+                r[m][n] = (i < B && k < B) ? A[i * B + k] : 0.0;
+            }
+        int failed = 0;
+        const int run_gj = bad == COL_OK;   // uniform (read after the last barrier)
+        for (int j = 0; j < B && run_gj; ++j) {
+            double* rj = rowj + (j & 1) * 96;   // rowj/colj hold 2 x 96 doubles (see smem layout)
+            double* cj = colj + (j & 1) * 96;
+            const int jm = j >> 3, jn = j >> 5;
+            if (ty == (j & 7)) {
+#pragma unroll
+                for (int m = 0; m < MR; ++m)
+                    if (m == jm)
+#pragma unroll
+                        for (int n = 0; n < 3; ++n) {
+                            const int k = tx + 32 * n;
+                            if (k < B) rj[k] = r[m][n];
+                        }
+            }
+            if (tx == (j & 31)) {
+#pragma unroll
+                for (int n = 0; n < 3; ++n)
+                    if (n == jn)
+#pragma unroll
+                        for (int m = 0; m < MR; ++m) {
+                            const int i = ty + 8 * m;
+                            if (i < B) cj[i] = r[m][n];
+                        }
+            }
             __syncthreads();
-            break;
-        }
-        const double p = 1.0 / piv;
-        for (int i = ty; i < B; i += 8) {
-            const double ci = colj[i] * p;
-            double* Ai = A + i * B;
-            for (int k = tx; k < B; k += 32) Ai[k] = fma(-ci, rowj[k], Ai[k]);
+            const double piv = rj[j];
+            if (!(piv > sh_tol) || !isfinite(piv)) {
+                failed = 1;   // uniform: every thread reads the same pivot
+                break;
+            }
+            const double p = 1.0 / piv;
+#pragma unroll
+            for (int m = 0; m < MR; ++m) {
+                const int i = ty + 8 * m;
+                const double ci = cj[i < B ? i : 0] * p;
+#pragma unroll
+                for (int n = 0; n < 3; ++n) {
+                    const int k = tx + 32 * n;
+                    const double rk = rj[k < B ? k : 0];
+                    double v = fma(-ci, rk, r[m][n]);
+                    if (i == j) v = (k == j) ? p : rk * p;
+                    else if (k == j) v = -ci;
+                    r[m][n] = v;
+                }
+            }
         }
         __syncthreads();
-        // row j, column j, pivot
-        for (int k = tid; k < B; k += blockDim.x) {
-            A[j * B + k] = rowj[k] * p;
-            A[k * B + j] = -colj[k] * p;
-        }
+        if (failed && tid == 0) bad = COL_NOT_SPD;
         __syncthreads();
-        if (tid == 0) A[j * B + j] = p;
+#pragma unroll
+        for (int m = 0; m < MR; ++m)
+#pragma unroll
+            for (int n = 0; n < 3; ++n) {
+                const int i = ty + 8 * m, k = tx + 32 * n;
+                if (i < B && k < B) A[i * B + k] = r[m][n];
+            }
         __syncthreads();
     }
     int st = bad;
@@ -1107,12 +1171,14 @@ __device__ __forceinline__ bool solve3(double K[3][3], double v[3], double x[3])
     return isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]);
 }
 
-__global__ void __launch_bounds__(128) k2_update(UpdateArgs a) {
+// 128 threads, <= 44 KB of shared memory at B = 72: 5 CTAs per SM, so the 598 columns
+// of a flightline run in one wave
+__global__ void __launch_bounds__(128, 5) k2_update(UpdateArgs a) {
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x;
     extern __shared__ double sAinv[];   // [B][B] A^-1 of this column (bulk copy)
     __shared__ uint64_t abar;
     __shared__ double sh_t[128], sh_h[128];
-    __shared__ double scratch[32 * 18];
+    __shared__ double scratch[(128 / 32) * 18];
     __shared__ double sh_coef[3];
     __shared__ double sh_s[3];
     __shared__ int sh_st;

@@ -138,6 +138,16 @@ int k1tc_be(int B);
 size_t k1tc_smem(int B);
 bool narrow(int B) { return B >= 4 && B <= 96 && B % 4 == 0; }
 int wide_blocks_per_sm(int B);
+void* k2_init_kernel(int B) {
+    switch ((B + 7) / 8) {
+#define SMF_K2I(n) \
+    case n: return reinterpret_cast<void*>(&k2_init<n>);
+        SMF_K2I(1) SMF_K2I(2) SMF_K2I(3) SMF_K2I(4) SMF_K2I(5) SMF_K2I(6) SMF_K2I(7) SMF_K2I(8) SMF_K2I(9)
+        SMF_K2I(10) SMF_K2I(11) SMF_K2I(12)
+#undef SMF_K2I
+        default: return nullptr;
+    }
+}
 
 bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     const int B = ctx->bands;
@@ -168,7 +178,7 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.be_full = p.k1tc ? k1tc_be(B) : 0;
     p.tpc1 = (N + p.T1 - 1) / p.T1;
     p.ttot1 = (long long)cols * p.tpc1;
-    p.G1 = (int)std::min<long long>(ctx->sm_count, p.ttot1);
+    p.G1 = (int)std::min<long long>(std::min(ctx->sm_count, kMaxSlots1), p.ttot1);
     p.S1 = 1;
     for (int b = 0; b < p.G1; ++b) {
         long long t0 = tile_begin(b, p.ttot1, p.G1), t1 = tile_begin(b + 1, p.ttot1, p.G1);
@@ -632,11 +642,14 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     ia.use_albedo = ctx->use_albedo;
     ia.stats_only = stats_only;
     ia.ridge_rel = ctx->ridge;
-    e = cudaFuncSetAttribute(k2_init, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem2);
+    void* k2fn = k2_init_kernel(p.B);
+    e = cudaFuncSetAttribute(k2fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem2);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k2_init smem attribute");
     {
         ProfScope ps(ctx, st, SMF_KERNEL_INIT);
-        k2_init<<<p.cols, 256, p.smem2, st>>>(ia);
+        void* args[] = {(void*)&ia};
+        e = cudaLaunchKernel(k2fn, dim3(p.cols), dim3(256), args, p.smem2, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k2_init launch");
     }
     ++launches;
     e = cudaGetLastError();
