@@ -392,7 +392,7 @@ int wide_blocks_per_sm(int B) {
 // tile (two buffers of kWideT3 rows) fits in shared memory
 bool supported(int B) {
     if (narrow(B)) return true;
-    return B >= 1 && k3w_j(B) > 0 && k3w_smem(B) <= 220 * 1024 &&
+    return B >= 1 && k3w_j(B) > 0 && B <= kWideNT2 * kWideMaxBPT2 && k3w_smem(B) <= 220 * 1024 &&
            k2w_init_smem(B) <= 200 * 1024 && k1w_smem(B, (B + 2 + 7) / 8 * 8) <= 220 * 1024;
 }
 

@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kWideNT1, 2) k1w_stats(WideStatsArgs a) {
 // ---------------------------------------------------------------- K2w init
 constexpr int kWideNT2 = 256;
 constexpr int kWideNTI = 512;     // k2w_init: a thread per matrix column (B <= 512) in the GJ updates
-constexpr int kWideMaxBPT2 = 8;   // bands per thread in k2w_update (B <= 2048)
+constexpr int kWideMaxBPT2 = 4;   // bands per thread in k2w_update (B <= 1024)
 constexpr int kGJ = 32;          // Gauss-Jordan block size
 
 struct WideInitArgs {
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
 // ---------------------------------------------------------------- K2w update
 __host__ inline size_t k2w_update_smem(int B) { return (size_t)(2 * B + 32 * 18) * 8; }
 
-__global__ void __launch_bounds__(kWideNT2) k2w_update(UpdateArgs a) {
+__global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
     extern __shared__ double w3_smem[];
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x, nt = blockDim.x;
     double* sh_t = w3_smem;        // [B]
