@@ -1327,6 +1327,7 @@ struct SweepArgs {
     int cols, N, B, tpc, G, S;
     long long ttot;
     int k, n_iter, use_sparsity, use_albedo, energy;
+    int bulk;   // wide sweep: every tile is a 16-byte aligned run of 16-byte multiples (TMA bulk copies)
     float eps, r_floor;
 };
 

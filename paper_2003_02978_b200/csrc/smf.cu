@@ -964,6 +964,8 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     sa.eps = (float)ctx->eps;
     sa.r_floor = (float)ctx->r_floor;
     sa.energy = ctx->energy;
+    sa.bulk = p.wide && ((uintptr_t)radiance % 16 == 0) && ((size_t)pixels * p.B % 4 == 0) &&
+              ((size_t)(pixels % kWideT3) * p.B % 4 == 0);
     UpdateArgs ua;
     ua.cs = cs;
     ua.part3 = sa.part3;

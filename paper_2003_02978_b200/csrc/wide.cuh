@@ -641,6 +641,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
     float* ms = zs + 32 * J;           // [32 J], zero beyond B
     __shared__ float2 sh_bs[kWideT3];   // (beta, sc) per pixel of the tile
     __shared__ float sh_aprev[kWideT3];
+    __shared__ uint64_t full[kWideS3];  // bulk path: one TMA bulk copy per tile
     __shared__ float sh_par[4];
     __shared__ int sh_st;
     __shared__ double red[kWideNT3 / 32][5];
@@ -651,6 +652,11 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
     const bool acce = accum || a.energy;   // partials written (energy: every sweep)
     // zero the ring once: the pads past the tile data stay zero
     for (size_t e = tid; e < kWideS3 * TF; e += kWideNT3) buf0[e] = 0.f;
+    if (tid == 0) {
+        for (int q2 = 0; q2 < kWideS3; ++q2) mbar_init(&full[q2], 1);
+        fence_mbar_init();
+    }
+    fence_proxy_async();
     __syncthreads();
 
     auto tile_src = [&](long long gt, int& rows) -> const float* {
@@ -663,7 +669,15 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
         int rows;
         const float* src = tile_src(tb + i, rows);
         float* dst = buf0 + (i % kWideS3) * TF + wide_tile_shift(src);
-        cp_async_floats(dst, src, rows * B, tid, kWideNT3);
+        if (a.bulk) {   // one TMA bulk copy (source 16-byte aligned, 16-byte multiple)
+            if (tid == 0) {
+                const uint32_t bytes = (uint32_t)rows * B * 4;
+                mbar_arrive_expect_tx(&full[i % kWideS3], bytes);
+                bulk_load(dst, src, bytes, &full[i % kWideS3]);
+            }
+        } else {
+            cp_async_floats(dst, src, rows * B, tid, kWideNT3);
+        }
     };
     // prologue: tiles 0 .. S-2 in flight (one commit group per tile, empty groups past the end)
     for (int i = 0; i < kWideS3 - 1; ++i) {
@@ -742,7 +756,10 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
         if (tid < kWideT3)
             sh_aprev[tid] = (a.k > 0 && a.use_sparsity && cst == COL_OK && tid < rows)
                                 ? a.enh[(size_t)c * a.N + p0 + tid] : 0.f;
-        cp_async_wait_ring();   // this thread's copies of tile i have landed
+        if (a.bulk)
+            mbar_wait(&full[i % kWideS3], (i / kWideS3) & 1);
+        else
+            cp_async_wait_ring();   // this thread's copies of tile i have landed
         __syncthreads();        // ... and everyone's; sh_aprev visible
         int rr_;
         const float* T = buf0 + (i % kWideS3) * TF + wide_tile_shift(tile_src(tb + i, rr_));
@@ -852,7 +869,8 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             for (int j = 0; j < NBT; ++j)
                 if (tid + j * kWideNT3 < B) acc[j] = s0[j] + s1[j];
         }
-        __syncthreads();   // slot i % S free for tile i + S
+        fence_proxy_async();   // generic reads of slot i % S before its async-proxy refill
+        __syncthreads();       // slot i % S free for tile i + S
     }
     if (cur >= 0 && acce) flush(cur - cfirst);
 }
