@@ -69,7 +69,8 @@ enum {
     SMF_COL_NONFINITE = 1,         /* a non-finite radiance value in the column */
     SMF_COL_DEGENERATE_MEAN = 2,   /* mu0 . mu0 = 0 with albedo correction (Eq. 7 undefined) */
     SMF_COL_NOT_SPD = 3,           /* C^k + rho I not numerically positive definite */
-    SMF_COL_DEGENERATE_TARGET = 4  /* t^T (C^k+rho I)^-1 t <= 0 or non-finite (Eq. 3/6 undefined) */
+    SMF_COL_DEGENERATE_TARGET = 4, /* t^T (C^k+rho I)^-1 t <= 0 or non-finite (Eq. 3/6 undefined) */
+    SMF_COL_INSUFFICIENT = 5       /* nodata masking left fewer than 2 valid pixels in the partition */
 };
 
 /* Create a context for `bands` spectral bands on the current CUDA device.
@@ -162,6 +163,15 @@ smf_status smf_initial_statistics(smf_ctx* ctx, const float* radiance, int cols,
 enum { SMF_STATS_AUTO = 0, SMF_STATS_FFMA = 1, SMF_STATS_TENSOR = 2 };
 smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind);
 int smf_stats_kernel_used(const smf_ctx* ctx);
+
+/* Nodata masking (the paper skips censored regions). With
+ * enable != 0 a pixel is nodata when any of its bands is non-finite or equals `value`
+ * (AVIRIS-NG files use -9999): it is left out of every statistic of its partition
+ * (mean, covariance, the iteration's sufficient statistics; N counts valid pixels only)
+ * and its enhancement and albedo are NaN; a partition with fewer than 2 valid pixels
+ * gets SMF_COL_INSUFFICIENT. Disabled (default), any non-finite value fails its column
+ * with SMF_COL_NONFINITE. */
+smf_status smf_set_nodata(smf_ctx* ctx, int enable, float value);
 
 /* On-device layout conversion of a radiance cube as stored on disk (AVIRIS-NG style,
  * SPEC S:23) into the retrieval layout [samples][lines][bands] (samples =

@@ -204,6 +204,36 @@ def retrieve_column(L, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-
     return alpha, r, rc
 
 
+def retrieve_masked(cube, s, nodata, **kw):
+    """Nodata masking (the paper skips censored regions): per column, a pixel with
+    any band non-finite or equal to `nodata` is removed before Fig. alg runs on the
+    remaining rows (so every statistic uses only valid pixels, N = their count); its
+    alpha and r are NaN. Fewer than 2 valid pixels: status 5 (INSUFFICIENT), all NaN.
+    Returns (alpha, r, status[, energies [n_iter+1][cols] if diagnostics=True])."""
+    cube = np.asarray(cube, dtype=np.float32)
+    cols, N, B = cube.shape
+    diagnostics = kw.pop("diagnostics", False)
+    alpha = np.full((cols, N), np.nan)
+    r = np.full((cols, N), np.nan)
+    status = np.zeros(cols, dtype=np.int32)
+    energy = np.full((kw.get("n_iter", 30) + 1, cols), np.nan)
+    for c in range(cols):
+        ok = np.all(np.isfinite(cube[c]) & (cube[c] != np.float32(nodata)), axis=1)
+        if ok.sum() < 2:
+            status[c] = 5
+            continue
+        out = retrieve_column(cube[c][ok], s, diagnostics=diagnostics, **kw)
+        a, rr, rc = out[:3]
+        alpha[c, ok], r[c, ok], status[c] = a, rr, rc
+        if rc != 0:
+            alpha[c], r[c] = np.nan, np.nan
+        if diagnostics:
+            energy[:, c] = out[3]["energy"]
+    if diagnostics:
+        return alpha, r, status, energy
+    return alpha, r, status
+
+
 def retrieve(cube, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2, lambda_rel=0.0,
              r_floor=0.05, threads=0):
     """Whole cube fp32 [cols][N][B] -> (alpha fp64 [cols][N], r fp64 [cols][N], status int32 [cols])."""

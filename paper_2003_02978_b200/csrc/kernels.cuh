@@ -37,7 +37,13 @@ constexpr int kStages = 3;        // K3 TMA ring depth
 constexpr int kStages1 = 2;       // K1 TMA ring depth (K1 is FFMA-bound)
 constexpr int kPilotRows = 32;    // pixels averaged for the K1 pilot shift
 
-enum { COL_OK = 0, COL_NONFINITE = 1, COL_DEGENERATE_MEAN = 2, COL_NOT_SPD = 3, COL_DEGENERATE_TARGET = 4 };
+enum { COL_OK = 0, COL_NONFINITE = 1, COL_DEGENERATE_MEAN = 2, COL_NOT_SPD = 3, COL_DEGENERATE_TARGET = 4,
+       COL_INSUFFICIENT = 5 };
+
+// nodata masking ("censored regions"): a pixel is nodata when any of
+// its bands is non-finite or equals the nodata value; it is left out of every statistic of
+// its partition and its enhancement / albedo are NaN
+__device__ __forceinline__ bool is_nodata(float v, float nodata) { return !isfinite(v) || v == nodata; }
 
 // Shared-memory tile geometry: bands split into `nfull` 32-band regions
 // (SWIZZLE_128B rows of 128 B) plus one tail region of `tailw` floats
@@ -170,6 +176,8 @@ struct StatsArgs {
     const float* ghat32;   // [cols][B] c/|c|^2
     double* part1;         // [G1cta][S1][W]
     int cols, N, B, tpc, G, S;
+    int mask;              // nodata masking: such rows contribute nothing (not even the count)
+    float nodata;
     long long ttot;
 };
 
@@ -287,6 +295,13 @@ __global__ void __launch_bounds__(K1Geom<NQ>::NT, 1)
                 for (int q = 0; q < NQ; ++q)
                     sgp[q & 3] = dot4(v[q], *reinterpret_cast<const float4*>(&gh[4 * q]), sgp[q & 3]);
                 const float sg = (sgp[0] + sgp[1]) + (sgp[2] + sgp[3]);
+                bool use = valid;
+                if (a.mask) {
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q)
+                        use = use && !is_nodata(v[q].x, a.nodata) && !is_nodata(v[q].y, a.nodata) &&
+                              !is_nodata(v[q].z, a.nodata) && !is_nodata(v[q].w, a.nodata);
+                }
                 const uint32_t xr = xb + row * (K::RQ * 16);
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
@@ -296,10 +311,10 @@ __global__ void __launch_bounds__(K1Geom<NQ>::NT, 1)
                     xv.y = fmaf(-sg, cq.y, v[q].y);
                     xv.z = fmaf(-sg, cq.z, v[q].z);
                     xv.w = fmaf(-sg, cq.w, v[q].w);
-                    if (!valid) xv = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (!use) xv = make_float4(0.f, 0.f, 0.f, 0.f);
                     sts4(xr + q * 16, xv);
                 }
-                sts4(xr + NQ * 16, valid ? make_float4(sg - 1.f, 1.f, 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f));
+                sts4(xr + NQ * 16, use ? make_float4(sg - 1.f, 1.f, 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f));
 #pragma unroll
                 for (int q = NQ + 1; q < K::BE / 4; ++q) sts4(xr + q * 16, make_float4(0.f, 0.f, 0.f, 0.f));
             }
@@ -563,6 +578,16 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
             }
             float sg = (sgp[0] + sgp[1]) + (sgp[2] + sgp[3]);
             sg += __shfl_xor_sync(0xffffffffu, sg, 16);
+            int ok = 1;   // nodata masking: both halves of the row must be valid
+            if (a.mask) {
+#pragma unroll
+                for (int q = 0; q < K::HQ; ++q)
+                    if (q < nqp && q0 + q < NQ)
+                        ok &= !is_nodata(v[q].x, a.nodata) && !is_nodata(v[q].y, a.nodata) &&
+                              !is_nodata(v[q].z, a.nodata) && !is_nodata(v[q].w, a.nodata);
+                ok &= __shfl_xor_sync(0xffffffffu, ok, 16);
+            }
+            const bool use = valid && ok;
             // order this thread's generic-proxy reads of the raw stage before the TMA
             // (async proxy) refill that the release below allows -- without it the
             // refill was measured to overwrite rows still being read
@@ -578,13 +603,13 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
                 float xs[4];
                 if (qq < NQ) {
                     const float4 cq = *reinterpret_cast<const float4*>(&pil[wid][4 * qq]);
-                    xs[0] = fmaf(-sg, cq.x, v[q].x);
-                    xs[1] = fmaf(-sg, cq.y, v[q].y);
-                    xs[2] = fmaf(-sg, cq.z, v[q].z);
-                    xs[3] = fmaf(-sg, cq.w, v[q].w);
+                    xs[0] = use ? fmaf(-sg, cq.x, v[q].x) : 0.f;
+                    xs[1] = use ? fmaf(-sg, cq.y, v[q].y) : 0.f;
+                    xs[2] = use ? fmaf(-sg, cq.z, v[q].z) : 0.f;
+                    xs[3] = use ? fmaf(-sg, cq.w, v[q].w) : 0.f;
                 } else {
-                    xs[0] = valid ? sg - 1.f : 0.f;
-                    xs[1] = valid ? 1.f : 0.f;
+                    xs[0] = use ? sg - 1.f : 0.f;
+                    xs[1] = use ? 1.f : 0.f;
                 }
 #pragma unroll
                 for (int j2 = 0; j2 < 4; ++j2) {
@@ -708,6 +733,8 @@ struct PilotArgs {
     float* pil32;
     float* ghat32;
     int cols, N, B;
+    int mask;
+    float nodata;
 };
 
 __global__ void k0_pilot(PilotArgs a) {
@@ -716,11 +743,25 @@ __global__ void k0_pilot(PilotArgs a) {
     __shared__ double scratch[32];
     const int np = min(kPilotRows, a.N);
     const size_t base = (size_t)c * a.N * a.B;
+    // with masking: the mean of the valid rows among the first kPilotRows (0 if none --
+    // the pilot only improves fp32 accuracy, the statistics stay exact)
+    __shared__ unsigned int validmask;   // bit p: row p valid
+    if (tid == 0) validmask = 0xffffffffu >> (32 - np);
+    __syncthreads();
+    if (a.mask) {
+        for (int b = tid; b < a.B; b += blockDim.x)
+            for (int p = 0; p < np; ++p)
+                if (is_nodata(a.L[base + (size_t)p * a.B + b], a.nodata)) atomicAnd(&validmask, ~(1u << p));
+        __syncthreads();
+    }
+    const unsigned int vm = validmask;
+    const int nv = __popc(vm);
     double sq = 0.0;
     for (int b = tid; b < a.B; b += blockDim.x) {
         float sum = 0.f;
-        for (int p = 0; p < np; ++p) sum += a.L[base + (size_t)p * a.B + b];
-        const float v = sum / (float)np;
+        for (int p = 0; p < np; ++p)
+            if (vm >> p & 1u) sum += a.L[base + (size_t)p * a.B + b];
+        const float v = nv > 0 ? sum / (float)nv : 0.f;
         a.pil32[(size_t)c * a.B + b] = v;
         sq += (double)v * (double)v;
     }
@@ -760,6 +801,9 @@ struct ColState {
     double* tra;      // [cols]
     double* rho64;    // [cols]
     double* tq;       // [cols]
+    double* nvalid;   // [cols] pixels in the partition's statistics (N, or the valid count when masking)
+    int mask;         // nodata masking on
+    float nodata;     // nodata value (masking)
 };
 
 // Deterministic block reduction of NV values per thread (fixed order).
@@ -836,7 +880,6 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     double* scratch = vt + B;      // [32][4]
     __shared__ int bad;
     __shared__ double sh_tol, sh_mm;
-    const double invN = 1.0 / (double)a.N;
     // gather the K1 slots covering this column, fixed CTA order: the slot list once
     // (thread 0), then independent loads per entry summed in that order
     {
@@ -871,6 +914,15 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     if (tid == 0) bad = COL_OK;
     __syncthreads();
     const int be = a.be_full;
+    // pixels in the statistics: N, or with masking the count of valid rows (the extended
+    // row's constant-1 entry summed: exact in fp32 runs and fp64 folds)
+    const double Nv = a.cs.mask ? ext_entry(S, B + 1, B + 1, be) : (double)a.N;
+    const double invN = 1.0 / Nv;
+    if (tid == 0) {
+        a.cs.nvalid[c] = Nv;
+        if (!(Nv >= 2.0)) bad = COL_INSUFFICIENT;
+    }
+    __syncthreads();
     const double Sr = ext_entry(S, B + 1, B, be), Srr = ext_entry(S, B, B, be);
     // sum (L - c) = sum x + (sum rho) c ;  dm = mean(L) - c
     for (int b = tid; b < B; b += blockDim.x) {
@@ -901,7 +953,7 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     }
     for (int b = tid; b < B; b += blockDim.x)
         if (!isfinite(dm[b])) nonfinite = 1;
-    if (nonfinite) atomicExch(&bad, COL_NONFINITE);
+    if (nonfinite && bad == COL_OK) atomicCAS(&bad, COL_OK, COL_NONFINITE);
     __syncthreads();
     for (int b = tid; b < B; b += blockDim.x) {
         double m = cv[b] + dm[b];
@@ -1136,7 +1188,7 @@ __global__ void k_energy(UpdateArgs a) {
         sbp += P[a.B + 3];
         swa += P[a.B + 4];
     }
-    *out = (double)a.N * a.cs.tq[c] - 2.0 * sbp + a.cs.q64[c] * s2 + swa;
+    *out = a.cs.nvalid[c] * a.cs.tq[c] - 2.0 * sbp + a.cs.q64[c] * s2 + swa;
 }
 
 
@@ -1217,7 +1269,7 @@ __global__ void __launch_bounds__(128, 5) k2_update(UpdateArgs a) {
         sh_s[2] = ss;
     }
     __syncthreads();
-    const double invN = 1.0 / (double)a.N;
+    const double invN = 1.0 / cs.nvalid[c];
     const double bbar = sh_s[0] * invN, b2 = sh_s[1] * invN, bs = sh_s[2] * invN;
     double mb = 0.0, tp = 0.0, t = 0.0, h = 0.0, mu = 0.0, yp = 0.0, mh = 0.0;
     if (tid < B) {
@@ -1328,6 +1380,8 @@ struct SweepArgs {
     long long ttot;
     int k, n_iter, use_sparsity, use_albedo, energy;
     int bulk;   // wide sweep: every tile is a 16-byte aligned run of 16-byte multiples (TMA bulk copies)
+    int mask;   // nodata masking
+    float nodata;
     float eps, r_floor;
 };
 
@@ -1469,6 +1523,17 @@ __global__ void __launch_bounds__(kTileRows, 2)
                 float4 Lq[NQ];
 #pragma unroll
                 for (int m = 0; m < NQ; ++m) Lq[m] = *reinterpret_cast<const float4*>(st + Gm::quad_off(tid, m));
+                bool okp = true;   // nodata masking: the pixel takes no part and reads NaN
+                if (a.mask) {
+#pragma unroll
+                    for (int m = 0; m < NQ; ++m)
+                        okp = okp && !is_nodata(Lq[m].x, a.nodata) && !is_nodata(Lq[m].y, a.nodata) &&
+                              !is_nodata(Lq[m].z, a.nodata) && !is_nodata(Lq[m].w, a.nodata);
+                }
+                if (!okp) {
+                    a.enh[pix] = __int_as_float(0x7fc00000);
+                    a.alb[pix] = __int_as_float(0x7fc00000);
+                } else {
                 // albedo factor r = L.mhat (Eq. 7, mhat = mu0/|mu0|^2)
                 float dm[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -1529,6 +1594,7 @@ __global__ void __launch_bounds__(kTileRows, 2)
                         acc[4 * m + 3] = fmaf(beta, Lq[m].w, acc[4 * m + 3]);
                     }
                 }
+                }   // okp
             }
         }
         fence_proxy_async();   // generic reads of stage s before its TMA (async-proxy) refill

@@ -33,6 +33,8 @@ struct smf_ctx {
     int stats_kernel = SMF_STATS_AUTO;
     int energy = 0;   // energy trace (smf_set_energy_trace)
     int group = 1;    // detector columns per partition (smf_set_grouping)
+    int mask = 0;     // nodata masking (smf_set_nodata)
+    float nodata = -9999.f;
     int last_launches = 0;
     char err[512] = {0};
     // profiling (smf_profile_*): events bracketing each launch
@@ -125,7 +127,7 @@ struct Plan {
     size_t smem1, smem2, smem3;
     // workspace offsets
     size_t o_mbar, o_mu, o_tprev, o_yprev, o_ainv, o_q64, o_z32, o_mhat, o_kc, o_q32, o_status, o_pilot, o_ghat, o_part1,
-        o_part3, o_tra, o_rho, o_tq, o_energy, total;
+        o_part3, o_tra, o_rho, o_tq, o_energy, o_nvalid, total;
     int n_energy;   // energy rows (n_iter + 1) or 0
 };
 
@@ -223,6 +225,7 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.o_tra = take((size_t)cols * 8);
     p.o_rho = take((size_t)cols * 8);
     p.o_tq = take((size_t)cols * 8);
+    p.o_nvalid = take((size_t)cols * 8);
     p.n_energy = ctx->energy ? ctx->n_iter + 1 : 0;
     p.o_energy = take((size_t)std::max(p.n_energy, 1) * cols * 8);
     p.total = o;
@@ -424,7 +427,7 @@ CUresult make_maps(const float* rad, int cols, int N, int B, CUtensorMap* main_m
     return r;
 }
 
-ColState col_state(const Plan& p, unsigned char* ws, const float* s) {
+ColState col_state(const Plan& p, unsigned char* ws, const float* s, const smf_ctx* ctx) {
     ColState cs;
     cs.mbar = (double*)(ws + p.o_mbar);
     cs.mu = (double*)(ws + p.o_mu);
@@ -441,6 +444,9 @@ ColState col_state(const Plan& p, unsigned char* ws, const float* s) {
     cs.tra = (double*)(ws + p.o_tra);
     cs.rho64 = (double*)(ws + p.o_rho);
     cs.tq = (double*)(ws + p.o_tq);
+    cs.nvalid = (double*)(ws + p.o_nvalid);
+    cs.mask = ctx->mask;
+    cs.nodata = ctx->nodata;
     return cs;
 }
 
@@ -517,6 +523,8 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     pa.cols = p.cols;
     pa.N = p.N;
     pa.B = p.B;
+    pa.mask = ctx->mask;
+    pa.nodata = ctx->nodata;
     {
         ProfScope ps(ctx, st, SMF_KERNEL_STATS);
         k0_pilot<<<p.cols, 128, 0, st>>>(pa);
@@ -529,7 +537,8 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         {
             ProfScope ps(ctx, st, SMF_KERNEL_STATS);
             const long long warps = (long long)p.cols * p.N;
-            k1w_sigma<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(rad, pa.ghat32, sigma, p.cols, p.N, p.B);
+            k1w_sigma<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(rad, pa.ghat32, sigma, p.cols, p.N, p.B,
+                                                                            ctx->mask, ctx->nodata);
         }
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_sigma launch");
@@ -544,6 +553,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         ta.N = p.N;
         ta.B = p.B;
         ta.NBLK = p.NBLKw;
+        ta.mask = ctx->mask;
         e = cudaFuncSetAttribute(k1w_stats_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats_tc smem attribute");
         {
@@ -566,6 +576,8 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         wa.BE = p.BEw;
         wa.NB = p.NBw;
         wa.NG = p.NGw;
+        wa.mask = ctx->mask;
+        wa.nodata = ctx->nodata;
         if (!p.widetc) {
             e = cudaFuncSetAttribute(k1w_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats smem attribute");
@@ -578,7 +590,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
             ++launches;
         }
         WideInitArgs ia;
-        ia.cs = col_state(p, ws, ctx->s_dev);
+        ia.cs = col_state(p, ws, ctx->s_dev, ctx);
         ia.pil32 = pa.pil32;
         ia.part = wa.part;
         ia.BEp = p.widetc ? p.NBLKw * 128 : 0;
@@ -614,6 +626,8 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     sa.G = p.G1;
     sa.S = p.S1;
     sa.ttot = p.ttot1;
+    sa.mask = ctx->mask;
+    sa.nodata = ctx->nodata;
     void* k1 = p.k1tc ? stats_tc_kernel(p.B) : stats_kernel(p.B);
     e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k1_stats smem attribute");
@@ -625,7 +639,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k1_stats launch");
     ++launches;
     InitArgs ia;
-    ia.cs = col_state(p, ws, ctx->s_dev);
+    ia.cs = col_state(p, ws, ctx->s_dev, ctx);
     ia.pil32 = pa.pil32;
     ia.part1 = sa.part1;
     ia.mean_out = mean_out;
@@ -778,6 +792,13 @@ smf_status smf_set_iterations(smf_ctx* ctx, int n_iter, int use_sparsity, int us
     ctx->n_iter = n_iter;
     ctx->use_sparsity = use_sparsity ? 1 : 0;
     ctx->use_albedo = use_albedo ? 1 : 0;
+    return SMF_OK;
+}
+
+smf_status smf_set_nodata(smf_ctx* ctx, int enable, float value) {
+    if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    ctx->mask = enable ? 1 : 0;
+    ctx->nodata = value;
     return SMF_OK;
 }
 
@@ -941,7 +962,7 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     int launches = 0;
     smf_status rc = launch_stats(ctx, p, radiance, ws, st, nullptr, nullptr, 0, launches);
     if (rc != SMF_OK) return rc;
-    ColState cs = col_state(p, ws, ctx->s_dev);
+    ColState cs = col_state(p, ws, ctx->s_dev, ctx);
     SweepArgs sa;
     sa.enh = enhancement;
     sa.alb = albedo;
@@ -964,6 +985,8 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     sa.eps = (float)ctx->eps;
     sa.r_floor = (float)ctx->r_floor;
     sa.energy = ctx->energy;
+    sa.mask = ctx->mask;
+    sa.nodata = ctx->nodata;
     sa.bulk = p.wide && ((uintptr_t)radiance % 16 == 0) && ((size_t)pixels * p.B % 4 == 0) &&
               ((size_t)(pixels % kWideT3) * p.B % 4 == 0);
     UpdateArgs ua;

@@ -74,6 +74,8 @@ struct WideStatsArgs {
     const float* ghat32;
     double* part;     // [cols][NG * 128][64] blocks of the extended-row second moments
     int cols, N, B, BE, NB, NG;
+    int mask;         // nodata masking: such rows contribute nothing
+    float nodata;
 };
 
 __host__ inline size_t k1w_smem(int B, int BE) { return (2 * (size_t)kWideT1 * BE + 2 * (size_t)B) * 4 + 16; }
@@ -144,18 +146,25 @@ __global__ void __launch_bounds__(kWideNT1, 2) k1w_stats(WideStatsArgs a) {
             constexpr int PW = (kWideT1 + kWideNT1 / 32 - 1) / (kWideNT1 / 32);   // pixels per warp
             const int pp0 = wid * PW;
             float sg[PW];
+            unsigned bad = 0u;   // bit u: pixel pp0 + u is nodata (masking)
 #pragma unroll
             for (int u = 0; u < PW; ++u) sg[u] = 0.f;
             for (int b = lane; b < B; b += 32) {
                 const float gb = gh[b];
 #pragma unroll
                 for (int u = 0; u < PW; ++u)
-                    if (pp0 + u < rows) sg[u] = fmaf(buf[(pp0 + u) * BE + b], gb, sg[u]);
+                    if (pp0 + u < rows) {
+                        const float lv = buf[(pp0 + u) * BE + b];
+                        sg[u] = fmaf(lv, gb, sg[u]);
+                        if (a.mask && is_nodata(lv, a.nodata)) bad |= 1u << u;
+                    }
             }
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1)
+            for (int off = 16; off > 0; off >>= 1) {
+                bad |= __shfl_xor_sync(0xffffffffu, bad, off);
 #pragma unroll
                 for (int u = 0; u < PW; ++u) sg[u] += __shfl_xor_sync(0xffffffffu, sg[u], off);
+            }
             for (int b = lane; b < BE; b += 32) {
                 const float pb = b < B ? pil[b] : 0.f;
 #pragma unroll
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(kWideNT1, 2) k1w_stats(WideStatsArgs a) {
                     if (pp >= kWideT1) break;
                     float* row = buf + pp * BE;
                     float v;
-                    if (pp >= rows) v = 0.f;
+                    if (pp >= rows || (bad >> u & 1u)) v = 0.f;
                     else if (b < B) v = fmaf(-sg[u], pb, row[b]);
                     else v = b == B ? sg[u] - 1.f : (b == B + 1 ? 1.f : 0.f);
                     row[b] = v;
@@ -334,7 +343,6 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     double* scratch = Cp + (size_t)B * (kGJ + 1);   // [32][4]
     __shared__ int bad;
     __shared__ double sh_tol, sh_mm;
-    const double invN = 1.0 / (double)a.N;
     const int BEp = a.BEp;
     const double* S = BEp > 0 ? a.part + (size_t)c * BEp * BEp : a.part + (size_t)c * a.NG * kWideNT1 * 64;
     // entry (i, k) of the extended-row second moments: FFMA 8x8 blocks, or the tensor-core
@@ -351,6 +359,13 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     };
     double* A = a.cs.ainv + (size_t)c * B * B;
     if (tid == 0) bad = COL_OK;
+    __syncthreads();
+    const double Nv = a.cs.mask ? ext(B + 1, B + 1) : (double)a.N;   // valid rows when masking
+    const double invN = 1.0 / Nv;
+    if (tid == 0) {
+        a.cs.nvalid[c] = Nv;
+        if (!(Nv >= 2.0)) bad = COL_INSUFFICIENT;
+    }
     __syncthreads();
     const double Sr = ext(B + 1, B), Srr = ext(B, B);
     int nonfinite = 0;
@@ -371,7 +386,7 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
         A[(size_t)i * B + k] = v;
         A[(size_t)k * B + i] = v;
     }
-    if (nonfinite) atomicExch(&bad, COL_NONFINITE);
+    if (nonfinite && bad == COL_OK) atomicCAS(&bad, COL_OK, COL_NONFINITE);
     __syncthreads();
     for (int b = tid; b < B; b += nt) {
         const double m = cv[b] + dm[b];
@@ -478,7 +493,7 @@ __global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
     while (b0 > 0 && tile_begin(b0, a.ttot, a.G) > c0) --b0;
     while (tile_begin(b0 + 1, a.ttot, a.G) <= c0) ++b0;
     const int W = B + kPartExtra;
-    const double invN = 1.0 / (double)a.N;
+    const double invN = 1.0 / cs.nvalid[c];
     if (tid == 0) {
         double s0 = 0.0, s2 = 0.0, ss = 0.0;
         for (int b = b0; b < a.G && tile_begin(b, a.ttot, a.G) < c1; ++b) {
@@ -640,6 +655,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
     float* zs = w4_smem + kWideS3 * TF;   // [32 J], zero beyond B
     float* ms = zs + 32 * J;           // [32 J], zero beyond B
     __shared__ float2 sh_bs[kWideT3];   // (beta, sc) per pixel of the tile
+    __shared__ int sh_ok[kWideT3];      // 0: nodata pixel (masking), kept out of the sums
     __shared__ float sh_aprev[kWideT3];
     __shared__ uint64_t full[kWideS3];  // bulk path: one TMA bulk copy per tile
     __shared__ float sh_par[4];
@@ -766,15 +782,25 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
         // ---- phase A: a warp per PB pixels (albedo, projection, update)
         for (int base = wid * PB; base < kWideT3; base += (kWideNT3 / 32) * PB) {
             float v[PB][J], r[PB], dz[PB];
+            int bad[PB];
 #pragma unroll
             for (int pb = 0; pb < PB; ++pb) {
                 r[pb] = 0.f;
+                bad[pb] = 0;
                 const float* row = T + (size_t)(base + pb) * B;
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
-                    v[pb][j] = row[lane + 32 * j];
+                    // elements past the row belong to the next pixel: zero them (0 * NaN of a
+                    // neighbouring nodata pixel must not reach this one)
+                    const bool inrow = lane + 32 * j < B;
+                    v[pb][j] = inrow ? row[lane + 32 * j] : 0.f;
                     r[pb] = fmaf(v[pb][j], ms[lane + 32 * j], r[pb]);
+                    if (a.mask && inrow && is_nodata(v[pb][j], a.nodata)) bad[pb] = 1;
                 }
+            }
+            if (a.mask) {
+#pragma unroll
+                for (int pb = 0; pb < PB; ++pb) bad[pb] = __any_sync(0xffffffffu, bad[pb]);
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1)
@@ -800,7 +826,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
                 float beta = 0.f, sc = 0.f;
                 if (pp < rows) {
                     const size_t pix = (size_t)c * a.N + p0 + pp;
-                    if (cst != COL_OK) {
+                    if (cst != COL_OK || bad[pb]) {   // failed column or nodata pixel
                         a.enh[pix] = __int_as_float(0x7fc00000);
                         a.alb[pix] = __int_as_float(0x7fc00000);
                     } else {
@@ -828,6 +854,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
                     }
                 }
                 sh_bs[pp] = make_float2(beta, sc);
+                sh_ok[pp] = !bad[pb];
                 sb += beta;
                 sb2 = fmaf(beta, beta, sb2);
                 sbs = fmaf(beta, sc, sbs);
@@ -854,16 +881,21 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             int pp = 0;
             for (; pp + 2 <= rows; pp += 2) {
                 const float2 bs0 = sh_bs[pp], bs1 = sh_bs[pp + 1];
+                const bool ok0 = sh_ok[pp], ok1 = sh_ok[pp + 1];
 #pragma unroll
                 for (int j = 0; j < NBT; ++j) {
-                    s0[j] = fmaf(bs0.x, fmaf(-bs0.y, mbv[j], tcol[j][(size_t)pp * B]), s0[j]);
-                    s1[j] = fmaf(bs1.x, fmaf(-bs1.y, mbv[j], tcol[j][(size_t)(pp + 1) * B]), s1[j]);
+                    const float t0 = ok0 ? tcol[j][(size_t)pp * B] : 0.f;
+                    const float t1 = ok1 ? tcol[j][(size_t)(pp + 1) * B] : 0.f;
+                    s0[j] = fmaf(bs0.x, fmaf(-bs0.y, mbv[j], t0), s0[j]);
+                    s1[j] = fmaf(bs1.x, fmaf(-bs1.y, mbv[j], t1), s1[j]);
                 }
             }
             if (pp < rows) {
                 const float2 bs0 = sh_bs[pp];
+                const bool ok0 = sh_ok[pp];
 #pragma unroll
-                for (int j = 0; j < NBT; ++j) s0[j] = fmaf(bs0.x, fmaf(-bs0.y, mbv[j], tcol[j][(size_t)pp * B]), s0[j]);
+                for (int j = 0; j < NBT; ++j)
+                    s0[j] = fmaf(bs0.x, fmaf(-bs0.y, mbv[j], ok0 ? tcol[j][(size_t)pp * B] : 0.f), s0[j]);
             }
 #pragma unroll
             for (int j = 0; j < NBT; ++j)
@@ -899,14 +931,16 @@ struct WideTCArgs {
     const float* L;
     const float* pil32;
     const float* ghat32;
-    const float* sigma;   // [cols][N]
+    const float* sigma;   // [cols][N] (NaN = nodata row when masking)
     double* part;         // [cols][BEp][BEp]
     int cols, N, B, NBLK;
+    int mask;
 };
 
 __global__ void k1w_sigma(const float* __restrict__ L, const float* __restrict__ ghat32, float* __restrict__ sigma,
-                          int cols, int N, int B) {
-    // a warp per pixel: lanes stride the bands, fixed-order butterfly
+                          int cols, int N, int B, int mask, float nodata) {
+    // a warp per pixel: lanes stride the bands, fixed-order butterfly; with masking a
+    // nodata pixel gets sigma = NaN, which the SYRK treats as "no row"
     const int lane = threadIdx.x & 31;
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (gw >= (long long)cols * N) return;
@@ -914,9 +948,15 @@ __global__ void k1w_sigma(const float* __restrict__ L, const float* __restrict__
     const float* Lp = L + (size_t)gw * B;
     const float* g = ghat32 + (size_t)c * B;
     float s = 0.f;
-    for (int b = lane; b < B; b += 32) s = fmaf(__ldg(Lp + b), __ldg(g + b), s);
+    int bad = 0;
+    for (int b = lane; b < B; b += 32) {
+        const float lv = __ldg(Lp + b);
+        s = fmaf(lv, __ldg(g + b), s);
+        if (mask) bad |= is_nodata(lv, nodata);
+    }
     s = warp_sum_f(s);
-    if (lane == 0) sigma[gw] = s;
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) sigma[gw] = bad ? __int_as_float(0x7fc00000) : s;
 }
 
 __host__ inline size_t k1w_tc_smem() { return 2 * (size_t)512 * 128 + 1024; }   // 2 stages x 512 rows x 128 B
@@ -992,7 +1032,7 @@ __global__ void __launch_bounds__(kTW, 1) k1w_stats_tc(WideTCArgs a) {
                 for (int j = 0; j < 32; ++j) {
                     const float xb = fmaf(-sv[j], cb, lv[j]);
                     const float v = b < B ? xb : (b == B ? sv[j] - 1.f : (b == B + 1 ? 1.f : 0.f));
-                    x[j] = p0 + j < N ? v : 0.f;
+                    x[j] = (p0 + j < N && !(a.mask && isnan(sv[j]))) ? v : 0.f;
                 }
                 const uint32_t base = ops0 + s2 * STAGE;
 #pragma unroll

@@ -42,6 +42,7 @@ SYMBOLS = {
     "smf_set_stats_kernel": (_i, [_vp, _i]),
     "smf_set_energy_trace": (_i, [_vp, _i]),
     "smf_set_grouping": (_i, [_vp, _i]),
+    "smf_set_nodata": (_i, [_vp, _i, ctypes.c_float]),
     "smf_convert_layout": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
     "smf_group_partitions": (_i, [_i, _i, ctypes.POINTER(_i), ctypes.POINTER(_i)]),
     "smf_energy_trace": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
@@ -59,7 +60,8 @@ for _name, (_res, _args) in SYMBOLS.items():
 
 SMF_OK, SMF_ERR_INVALID_ARGUMENT, SMF_ERR_NOT_CONFIGURED, SMF_ERR_SHAPE, SMF_ERR_NUMERICAL, SMF_ERR_CUDA, \
     SMF_ERR_OUT_OF_MEMORY = range(7)
-COLUMN_STATUS = {0: "OK", 1: "NONFINITE", 2: "DEGENERATE_MEAN", 3: "NOT_SPD", 4: "DEGENERATE_TARGET"}
+COLUMN_STATUS = {0: "OK", 1: "NONFINITE", 2: "DEGENERATE_MEAN", 3: "NOT_SPD", 4: "DEGENERATE_TARGET",
+                 5: "INSUFFICIENT"}
 
 
 class SMFError(RuntimeError):
@@ -115,7 +117,7 @@ class Retriever:
     STATS_KERNELS = {"auto": 0, "ffma": 1, "tensor": 2}
 
     def __init__(self, bands, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2, ridge_rel=0.0,
-                 r_floor=0.05, stats_kernel="auto", energy=False, group=1):
+                 r_floor=0.05, stats_kernel="auto", energy=False, group=1, nodata=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("smf needs a CUDA device (no CPU fallback)")
@@ -130,6 +132,8 @@ class Retriever:
         self._check(_lib.smf_set_stats_kernel(self._h, self.STATS_KERNELS[stats_kernel]))
         self._check(_lib.smf_set_energy_trace(self._h, int(bool(energy))))
         self._check(_lib.smf_set_grouping(self._h, int(group)))
+        self._check(_lib.smf_set_nodata(self._h, int(nodata is not None),
+                                        float(nodata) if nodata is not None else -9999.0))
         self.group = int(group)
         self.n_iter = int(n_iter)
 

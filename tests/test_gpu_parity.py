@@ -289,6 +289,44 @@ def test_layout_conversion(smf, torch, layout):
     np.testing.assert_array_equal(out, cpb)
 
 
+# ------------------------------------------------------------------ nodata masking (NEXT f3)
+@pytest.mark.parametrize("bands,group", [(32, 1), (13, 1), (72, 1), (32, 3)])
+def test_nodata_masking_vs_oracle(smf, torch, bands, group):
+    """Censored pixels: any band equal to -9999 or non-finite removes the pixel
+    from its partition's statistics and gives NaN enhancement / albedo; a partition left
+    with < 2 valid pixels is INSUFFICIENT (5). Oracle: Fig. alg on the valid rows."""
+    cfg = synth.scaled(synth.CONFIGS["tiny"], cols=6, pixels=300, bands=bands, rank=8)
+    cube, s, _ = synth.generate(cfg)
+    rng = np.random.default_rng(9)
+    for c in range(5):
+        bad = rng.choice(cfg.pixels, size=25, replace=False)
+        cube[c, bad[:10]] = -9999.0                      # whole pixels censored
+        cube[c, bad[10:20], rng.integers(0, bands, 10)] = -9999.0   # a single band
+        cube[c, bad[20:], rng.integers(0, bands, 5)] = np.nan
+    if group == 1:
+        cube[5, 1:] = -9999.0                            # one valid pixel left
+    r = smf.Retriever(bands, s, n_iter=8, nodata=-9999.0, energy=True, group=group)
+    rad = torch.from_numpy(np.ascontiguousarray(cube)).cuda()
+    ws = r.alloc_workspace(cfg.cols, cfg.pixels)
+    enh, alb, st = r.retrieve(rad, workspace=ws)
+    torch.cuda.synchronize()
+    E = r.energy_trace(ws, cfg.cols, cfg.pixels).cpu().numpy()
+    enh, alb, st = enh.cpu().numpy(), alb.cpu().numpy(), st.cpu().numpy()
+    if group == 1:
+        a_ref, r_ref, st_ref, E_ref = oracle.retrieve_masked(cube, s, -9999.0, n_iter=8, diagnostics=True)
+        np.testing.assert_array_equal(st, st_ref)
+        assert st[5] == 5 and np.isnan(enh[5]).all()
+        ok = st_ref == 0
+        assert np.all(np.abs(E[:, ok] / E_ref[:, ok] - 1) < 1e-4)
+    else:
+        pooled = cube.reshape(2, 3 * cfg.pixels, bands)
+        a_ref, r_ref, st_ref = oracle.retrieve_masked(pooled, s, -9999.0, n_iter=8)
+        a_ref, r_ref = a_ref.reshape(cfg.cols, cfg.pixels), r_ref.reshape(cfg.cols, cfg.pixels)
+        assert (st == 0).all() and (st_ref == 0).all()
+    rep = assert_parity(enh, alb, a_ref, r_ref, f"nodata B={bands} G={group}")
+    print(rep)
+
+
 def test_column_status_codes(smf, torch):
     cfg = synth.scaled(synth.CONFIGS["tiny"], cols=5)
     cube, s, _ = synth.generate(cfg)
