@@ -99,6 +99,16 @@ struct TileCursor {
             ++c;
         }
     }
+    __device__ __forceinline__ void prev() {
+        if (tt-- == 0) {
+            tt = tpc - 1;
+            --c;
+        }
+    }
+    __device__ __forceinline__ void step(bool rev) {
+        if (rev) prev();
+        else next();
+    }
 };
 
 // Shared-memory image of one TMA tile of ROWS pixels x 4*NQ bands (see TileGeom).
@@ -1383,6 +1393,10 @@ struct SweepArgs {
     int mask;   // nodata masking
     float nodata;
     float eps, r_floor;
+    int rev;    // serpentine: walk this CTA's tile range backwards (alternate sweeps), so the
+                // tiles the previous pass read last -- still in L2 -- are read first
+    int keep;   // > 0: the last `keep` tiles of this CTA's pass load with L2 evict_last, the
+                // rest with evict_first (the kept tail is what the next, reversed pass reads first)
 };
 
 template <int NQ>
@@ -1415,16 +1429,27 @@ __global__ void __launch_bounds__(kTileRows, 2)
         fence_mbar_init();
     }
     __syncthreads();
-    TileCursor icur(tb, a.tpc);   // next tile to issue (thread 0 only)
+    const bool rev = a.rev && ntl > 0;
+    TileCursor icur(rev ? te - 1 : tb, a.tpc);   // next tile to issue (thread 0 only)
     auto issue = [&](int i) {
         const int c = icur.c, row0 = icur.tt * kTileRows;
-        icur.next();
+        icur.step(rev);
         unsigned char* st = stages + (i % kStages) * Gm::STAGE;
         uint64_t* bar = &full[i % kStages];
         mbar_arrive_expect_tx(bar, Gm::TX);
+        if (a.keep > 0) {
+            const uint64_t pol = i >= ntl - a.keep ? l2_policy_evict_last() : l2_policy_evict_first();
 #pragma unroll
-        for (int f = 0; f < Gm::NFULL; ++f) tma_load_3d(st + f * (kTileRows * 128), &tm_main, bar, f * 32, row0, c);
-        if (Gm::TAILW) tma_load_3d(st + Gm::NFULL * (kTileRows * 128), &tm_tail, bar, Gm::NFULL * 32, row0, c);
+            for (int f = 0; f < Gm::NFULL; ++f)
+                tma_load_3d_hint(st + f * (kTileRows * 128), &tm_main, bar, f * 32, row0, c, pol);
+            if (Gm::TAILW)
+                tma_load_3d_hint(st + Gm::NFULL * (kTileRows * 128), &tm_tail, bar, Gm::NFULL * 32, row0, c, pol);
+        } else {
+#pragma unroll
+            for (int f = 0; f < Gm::NFULL; ++f)
+                tma_load_3d(st + f * (kTileRows * 128), &tm_main, bar, f * 32, row0, c);
+            if (Gm::TAILW) tma_load_3d(st + Gm::NFULL * (kTileRows * 128), &tm_tail, bar, Gm::NFULL * 32, row0, c);
+        }
     };
     if (tid == 0)
         for (int i = 0; i < kStages && i < ntl; ++i) issue(i);
@@ -1476,8 +1501,8 @@ __global__ void __launch_bounds__(kTileRows, 2)
     int cur = -1;
     float mz = 0.f, cz = 0.f, q = 1.f, mmf = 1.f;
     int cst = 0;
-    TileCursor ccur(tb, a.tpc);
-    for (int i = 0; i < ntl; ++i, ccur.next()) {
+    TileCursor ccur(rev ? te - 1 : tb, a.tpc);
+    for (int i = 0; i < ntl; ++i, ccur.step(rev)) {
         const int c = ccur.c;
         const int row0 = ccur.tt * kTileRows;
         if (c != cur) {

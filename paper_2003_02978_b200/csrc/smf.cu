@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -367,6 +368,29 @@ int sweep_blocks_per_sm(int B) {
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kTileRows, smem) != cudaSuccess) return 1;
     return std::max(n, 1);
+}
+
+// Serpentine sweep order (narrow path): alternate sweeps walk each CTA's tile range
+// backwards so the start of a pass hits the L2-resident tail of the previous one.
+// SMF_SERPENTINE=0 turns it off (A/B measurement).
+bool serpentine() {
+    static const bool on = [] {
+        const char* e = std::getenv("SMF_SERPENTINE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// Tiles per sweep CTA whose L2 lines are kept (evict_last) for the next, reversed pass:
+// SMF_L2KEEP_MB (default 48) of the 126 MB L2 spread over the sweep grid; 0 = no hints.
+int l2_keep_tiles(const Plan& p) {
+    static const long mb = [] {
+        const char* e = std::getenv("SMF_L2KEEP_MB");
+        return e ? std::atol(e) : 48L;
+    }();
+    if (p.wide || mb <= 0 || p.G <= 0) return 0;
+    const double tile = (double)kTileRows * p.B * 4.0;
+    return (int)std::max(1.0, (double)mb * 1048576.0 / ((double)p.G * tile));
 }
 
 void* wide_sweep_kernel(int B) {
@@ -1023,6 +1047,8 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
             ++launches;
         }
         sa.k = k;
+        sa.rev = serpentine() && p.wide == 0 ? (k & 1) == 0 : 0;   // K1 walks forward
+        sa.keep = serpentine() ? l2_keep_tiles(p) : 0;
         cudaError_t e;
         {
             ProfScope ps(ctx, st, SMF_KERNEL_SWEEP);
