@@ -314,7 +314,8 @@ def main():
         raise SystemExit(f"column {first_fail} failed")
 
     # ---- timed region (device time, CUDA events on the launching stream)
-    r.profile_enable(True)
+    prof_in_timed = os.environ.get("SMF_BENCH_PROF", "0") != "0"
+    r.profile_enable(prof_in_timed)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         torch.distributed.barrier()
@@ -328,6 +329,14 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
+    if not prof_in_timed:
+        # per-kernel event brackets break the programmatic-dependent-launch overlap of
+        # consecutive kernels, so the kernel durations come from a second, bracketed pass
+        # of the same K steps right after the timed region
+        r.profile_enable(True)
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
     prof = r.profile_read()
     r.profile_enable(False)
     launches_per_step = r.last_launch_count
@@ -403,7 +412,12 @@ def main():
                              "avg_launch_us": k3_avg_s * 1e6, "peak_source": peak_src,
                              "step_achieved_gbs": step_achieved, "step_frac": step_achieved / peak,
                              "step_algorithmic_bytes": total_bytes,
-                             "kernel_time_share": kernel_share},
+                             "kernel_time_share": kernel_share,
+                             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+                             "kernel_durations": "CUDA events bracketing each launch on its stream, "
+                                                 + ("inside the timed region" if prof_in_timed else
+                                                    "in a second pass of the same K steps right after "
+                                                    "the (unbracketed) timed region")},
                 "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk.summary(),
                 "gpu_launches": launches_per_step * args.steps}

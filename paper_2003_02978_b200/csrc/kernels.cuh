@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(K1Geom<NQ>::NT, 1)
     }
     for (int i = tid; i < K::W; i += K::NT) buf[i] = 0.0;
     __syncthreads();
+    griddep_wait();
 
     if (wid == K::NMW) {
         // ===================== producer warp: TMA + extended-row rewrite =====================
@@ -535,6 +536,7 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_sh;
+    griddep_wait();
 
     if (wid < 8) {
         // ===================== transform: raw tile -> [H | L] operand image =====================
@@ -878,6 +880,7 @@ constexpr int kMaxSlots1 = 256;   // >= the statistics grid (one CTA per SM)
 template <int MR>
 __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
     extern __shared__ double sm2[];
+    griddep_wait();
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x;
     double* A = sm2;               // [B][B]
     double* S = A + B * B;         // [W1] extended-row sums of this column
@@ -1244,6 +1247,7 @@ __global__ void __launch_bounds__(128, 5) k2_update(UpdateArgs a) {
     __shared__ double sh_coef[3];
     __shared__ double sh_s[3];
     __shared__ int sh_st;
+    griddep_wait();
     ColState& cs = a.cs;
     const int st0 = cs.status[c];
     if (st0 != COL_OK) return;   // uniform per block
@@ -1452,7 +1456,8 @@ __global__ void __launch_bounds__(kTileRows, 2)
         }
     };
     if (tid == 0)
-        for (int i = 0; i < kStages && i < ntl; ++i) issue(i);
+        for (int i = 0; i < kStages && i < ntl; ++i) issue(i);   // the cube is read-only: no wait
+    griddep_wait();
 
     float acc[B4];
 #pragma unroll

@@ -83,6 +83,11 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
         : "memory");
 }
 
+// Programmatic dependent launch: block until the preceding kernel in the stream has
+// completed and its memory is visible (returns at once for a normal launch). Everything
+// before it may only touch this kernel's own shared memory or read-only inputs.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

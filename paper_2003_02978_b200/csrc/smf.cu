@@ -370,6 +370,33 @@ int sweep_blocks_per_sm(int B) {
     return std::max(n, 1);
 }
 
+// Programmatic dependent launch (SMF_PDL=0 turns it off): the kernel may be scheduled
+// while its predecessor in the stream drains; it runs its prologue (barrier init, TMEM
+// allocation, the first TMA loads of the read-only cube) and then blocks in griddep_wait()
+// until the predecessor has completed. Only kernels that call griddep_wait() use it.
+bool pdl_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("SMF_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
+    if (!pdl_on()) return cudaLaunchKernel(fn, grid, block, args, smem, st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 // Serpentine sweep order (narrow path): alternate sweeps walk each CTA's tile range
 // backwards so the start of a pass hits the L2-resident tail of the previous one.
 // SMF_SERPENTINE=0 turns it off (A/B measurement).
@@ -658,7 +685,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     {
         ProfScope ps(ctx, st, SMF_KERNEL_STATS);
         void* args[] = {(void*)&mm, (void*)&tm, (void*)&sa};
-        e = cudaLaunchKernel(k1, dim3(p.G1), dim3(p.NT1), args, p.smem1, st);
+        e = launch_pdl(k1, dim3(p.G1), dim3(p.NT1), args, p.smem1, st);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k1_stats launch");
     ++launches;
@@ -686,7 +713,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     {
         ProfScope ps(ctx, st, SMF_KERNEL_INIT);
         void* args[] = {(void*)&ia};
-        e = cudaLaunchKernel(k2fn, dim3(p.cols), dim3(256), args, p.smem2, st);
+        e = launch_pdl(k2fn, dim3(p.cols), dim3(256), args, p.smem2, st);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k2_init launch");
     }
     ++launches;
@@ -1040,7 +1067,10 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
                 if (p.wide)
                     k2w_update<<<cols, kWideNT2, smem_up, st>>>(ua);
                 else
-                    k2_update<<<cols, 128, smem_up, st>>>(ua);
+                {
+                    void* args[] = {(void*)&ua};
+                    launch_pdl(reinterpret_cast<const void*>(&k2_update), dim3(cols), dim3(128), args, smem_up, st);
+                }
             }
             e0 = cudaGetLastError();
             if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k2_update launch");
@@ -1058,7 +1088,7 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
                 e = cudaLaunchKernel(kfn, dim3(p.G), dim3(kWideNT3), args, p.smem3, st);
             } else {
                 void* args[] = {(void*)&mm, (void*)&tm, (void*)&sa};
-                e = cudaLaunchKernel(kfn, dim3(p.G), dim3(kTileRows), args, p.smem3, st);
+                e = launch_pdl(kfn, dim3(p.G), dim3(kTileRows), args, p.smem3, st);
             }
         }
         if (e != cudaSuccess) return cuda_fail(ctx, e, "sweep launch");
