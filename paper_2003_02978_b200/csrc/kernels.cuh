@@ -455,6 +455,10 @@ constexpr int kTileTC = 64;       // pixels per tile (8 MMA K-steps of 8)
 #ifndef SMF_K1TC_FLUSH
 #define SMF_K1TC_FLUSH 4
 #endif
+#ifndef SMF_K1TC_EXP
+#define SMF_K1TC_EXP 0   // bisection builds only (DESIGN 5.5): 1 = no MMA, 2 = no operand stores,
+                         // 4 = no fp64 fold, 8 = no transform work (barrier hand-offs only)
+#endif
 constexpr int kFlushTC = SMF_K1TC_FLUSH;   // tiles per fp32 TMEM accumulation run (256 pixels)
 constexpr int kOpStagesTC = 2;    // operand ring depth (= transform pairs)
 
@@ -579,6 +583,14 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
             const int s = i % K::RS, o = i % kOpStagesTC;
             const bool valid = row0 + row < a.N;   // rows beyond N arrive zero-filled by TMA
             mbar_wait(&raw_full[s], (i / K::RS) & 1);
+            if (SMF_K1TC_EXP & 8) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&raw_empty[s]);
+                if (i >= kOpStagesTC) mbar_wait(&op_empty[o], ((i / kOpStagesTC) - 1) & 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&op_full[o]);
+                continue;
+            }
             float4 v[K::HQ];
             float sgp[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -632,8 +644,10 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
                     const float l = x - h;   // exact; the MMA reads it as tf32 (low-part rounding
                                              // measured to make no difference)
                     const uint32_t ad = ob + abase[jb & 7] + (uint32_t)jb * 128;
-                    sts1(ad, h);
-                    sts1(ad + (uint32_t)K::BE * 128, l);
+                    if (!(SMF_K1TC_EXP & 2)) {
+                        sts1(ad, h);
+                        sts1(ad + (uint32_t)K::BE * 128, l);
+                    }
                 }
             }
             fence_proxy_async();   // generic-proxy smem writes -> visible to the tensor core
@@ -662,7 +676,7 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
             for (int n0 = 0; n0 < K::BE; n0 += 16) {
                 float v[16], u[16];
                 tmem_ld16x2(t0 + n0, t0 + K::BE + n0, v, u);
-                if (live) {
+                if (live && !(SMF_K1TC_EXP & 4)) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) arow[n0 + j] += (double)v[j] + 2.0 * (double)u[j];
                 }
@@ -718,7 +732,8 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
 #pragma unroll
                 for (int ks = 0; ks < kTileTC / 8; ++ks) {
                     const uint64_t d = umma_desc(sa + (ks >> 2) * K::REG + (ks & 3) * 32, 16, 1024, 2);
-                    mma_tf32(tmem + (uint32_t)(ab * K::NCOL), d, d, K::IDESC, (fresh && ks == 0) ? 0u : 1u);
+                    if (!(SMF_K1TC_EXP & 1))
+                        mma_tf32(tmem + (uint32_t)(ab * K::NCOL), d, d, K::IDESC, (fresh && ks == 0) ? 0u : 1u);
                 }
                 fresh = false;
                 mma_commit(&op_empty[o]);

@@ -8,7 +8,7 @@ rng = np.random.default_rng(0)
 cube = torch.empty((cfg.cols, cfg.pixels, cfg.bands), dtype=torch.float32, device="cuda")
 cube.uniform_(0.5, 1.5)
 s = -np.abs(rng.standard_normal(cfg.bands)).astype(np.float32) * 1e-5
-for k in ("tensor", "ffma"):
+for k in os.environ.get("K1_KERNELS", "tensor,ffma").split(","):
     r = smf.Retriever(cfg.bands, s, stats_kernel=k)
     ws = r.alloc_workspace(cfg.cols, cfg.pixels)
     for _ in range(3): r.initial_statistics(cube, workspace=ws)
