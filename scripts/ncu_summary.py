@@ -39,7 +39,8 @@ def to_bytes(v, u):
 
 if __name__ == "__main__":
     outdir, config, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
-    traffic_path = os.path.join(os.path.dirname(outdir.rstrip("/")), "traffic.json")
+    traffic_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                                "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     for rep in reps:
         name = os.path.basename(rep).replace(".ncu-rep", "")
