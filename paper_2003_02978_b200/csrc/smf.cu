@@ -420,16 +420,21 @@ int l2_keep_tiles(const Plan& p) {
     return (int)std::max(1.0, (double)mb * 1048576.0 / ((double)p.G * tile));
 }
 
-void* wide_sweep_kernel(int B) {
+template <bool MASK>
+void* wide_sweep_kernel_t(int B) {
     switch (k3w_j(B)) {
-        case 2: return reinterpret_cast<void*>(&k3w_sweep<2>);
-        case 4: return reinterpret_cast<void*>(&k3w_sweep<4>);
-        case 8: return reinterpret_cast<void*>(&k3w_sweep<8>);
-        case 14: return reinterpret_cast<void*>(&k3w_sweep<14>);
-        case 20: return reinterpret_cast<void*>(&k3w_sweep<20>);
-        case 28: return reinterpret_cast<void*>(&k3w_sweep<28>);
+        case 2: return reinterpret_cast<void*>(&k3w_sweep<2, MASK>);
+        case 4: return reinterpret_cast<void*>(&k3w_sweep<4, MASK>);
+        case 8: return reinterpret_cast<void*>(&k3w_sweep<8, MASK>);
+        case 14: return reinterpret_cast<void*>(&k3w_sweep<14, MASK>);
+        case 20: return reinterpret_cast<void*>(&k3w_sweep<20, MASK>);
+        case 28: return reinterpret_cast<void*>(&k3w_sweep<28, MASK>);
         default: return nullptr;
     }
+}
+
+void* wide_sweep_kernel(int B, bool mask = false) {
+    return mask ? wide_sweep_kernel_t<true>(B) : wide_sweep_kernel_t<false>(B);
 }
 
 int wide_blocks_per_sm(int B) {
@@ -1057,7 +1062,7 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     void* ufn = p.wide ? reinterpret_cast<void*>(&k2w_update) : reinterpret_cast<void*>(&k2_update);
     cudaError_t e0 = cudaFuncSetAttribute(ufn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_up);
     if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k2_update smem attribute");
-    void* kfn = p.wide ? wide_sweep_kernel(p.B) : sweep_kernel(p.B);
+    void* kfn = p.wide ? wide_sweep_kernel(p.B, ctx->mask != 0) : sweep_kernel(p.B);
     e0 = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem3);
     if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k3_sweep smem attribute");
     for (int k = 0; k <= ctx->n_iter; ++k) {

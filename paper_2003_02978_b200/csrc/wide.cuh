@@ -644,7 +644,9 @@ __host__ inline size_t k3w_smem(int B) {
 // J = elements per lane of a pixel row (B <= 32 J); each warp processes PB pixels at
 // once (their dot products interleaved for ILP), keeping the row in registers between
 // the albedo pass and the projection pass.
-template <int J>
+// MASK: nodata masking compiled in (the checks cost ~45 % of the sweep's time when
+// present, so the common no-masking launch uses the MASK = false instance)
+template <int J, bool MASK>
 __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const float* L) {
     constexpr int PB = kWideT3 / (kWideNT3 / 32);   // pixels per warp per tile
     constexpr int NBT = (32 * J + kWideNT3 - 1) / kWideNT3;   // bands per thread in phase B
@@ -792,13 +794,14 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
                 for (int j = 0; j < J; ++j) {
                     // elements past the row belong to the next pixel: zero them (0 * NaN of a
                     // neighbouring nodata pixel must not reach this one)
-                    const bool inrow = lane + 32 * j < B;
+                    // (without masking a non-finite neighbour makes the column NONFINITE anyway)
+                    const bool inrow = !MASK || lane + 32 * j < B;
                     v[pb][j] = inrow ? row[lane + 32 * j] : 0.f;
                     r[pb] = fmaf(v[pb][j], ms[lane + 32 * j], r[pb]);
-                    if (a.mask && inrow && is_nodata(v[pb][j], a.nodata)) bad[pb] = 1;
+                    if (MASK && inrow && is_nodata(v[pb][j], a.nodata)) bad[pb] = 1;
                 }
             }
-            if (a.mask) {
+            if (MASK) {
 #pragma unroll
                 for (int pb = 0; pb < PB; ++pb) bad[pb] = __any_sync(0xffffffffu, bad[pb]);
             }
@@ -881,7 +884,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             int pp = 0;
             for (; pp + 2 <= rows; pp += 2) {
                 const float2 bs0 = sh_bs[pp], bs1 = sh_bs[pp + 1];
-                const bool ok0 = sh_ok[pp], ok1 = sh_ok[pp + 1];
+                const bool ok0 = !MASK || sh_ok[pp], ok1 = !MASK || sh_ok[pp + 1];
 #pragma unroll
                 for (int j = 0; j < NBT; ++j) {
                     const float t0 = ok0 ? tcol[j][(size_t)pp * B] : 0.f;
@@ -892,7 +895,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             }
             if (pp < rows) {
                 const float2 bs0 = sh_bs[pp];
-                const bool ok0 = sh_ok[pp];
+                const bool ok0 = !MASK || sh_ok[pp];
 #pragma unroll
                 for (int j = 0; j < NBT; ++j)
                     s0[j] = fmaf(bs0.x, fmaf(-bs0.y, mbv[j], ok0 ? tcol[j][(size_t)pp * B] : 0.f), s0[j]);
