@@ -627,7 +627,6 @@ __global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
 constexpr int kWideT3 = 16;       // pixels per K3w tile
 constexpr int kWideS3 = 2;        // K3w cp.async ring depth (tiles in flight)
 constexpr int kWideNT3 = 128;     // threads per K3w CTA (4 warps; 4 CTAs per SM)
-constexpr int kWideMaxBPT = 8;    // bands per thread in the beta L' accumulation (B <= 2048)
 
 // floats per tile buffer: 32 rows + 4 floats of alignment shift + 32 floats of zero pad
 // (the register pass reads up to 32 J - B floats past a row; the pad keeps that finite)
@@ -641,28 +640,31 @@ __host__ inline size_t k3w_smem(int B) {
     return (kWideS3 * k3w_tile_floats(B) + 2 * (size_t)(J > 0 ? 32 * J : B)) * 4 + 16;
 }
 
-// J = elements per lane of a pixel row (B <= 32 J); each warp processes PB pixels at
-// once (their dot products interleaved for ILP), keeping the row in registers between
-// the albedo pass and the projection pass.
+// J = elements per lane of a pixel row (B <= 32 J). A warp processes PB pixels at once
+// (their dot products interleaved for ILP): lane l holds bands l + 32 j of each row in
+// registers from the albedo dot through the projection to the sum of beta L' (the
+// statistics for k + 1), so the tile is read from shared memory once; the xor
+// butterflies leave every lane with the full dots, so all lanes evaluate the pixel update
+// identically and lane 0 stores it. Per-lane sums are combined across the warps in a
+// fixed order (fp64) at each column-slot flush.
 // MASK: nodata masking compiled in (the checks cost ~45 % of the sweep's time when
 // present, so the common no-masking launch uses the MASK = false instance)
 template <int J, bool MASK>
 __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const float* L) {
-    constexpr int PB = kWideT3 / (kWideNT3 / 32);   // pixels per warp per tile
-    constexpr int NBT = (32 * J + kWideNT3 - 1) / kWideNT3;   // bands per thread in phase B
+    constexpr int NW = kWideNT3 / 32;
+    constexpr int PB = J >= 20 ? 1 : 2;   // pixels per warp pass (registers: PB x J row elements)
     extern __shared__ __align__(16) float w4_smem[];
     const int B = a.B, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const size_t TF = k3w_tile_floats(B);
     float* buf0 = w4_smem;
     float* zs = w4_smem + kWideS3 * TF;   // [32 J], zero beyond B
     float* ms = zs + 32 * J;           // [32 J], zero beyond B
-    __shared__ float2 sh_bs[kWideT3];   // (beta, sc) per pixel of the tile
-    __shared__ int sh_ok[kWideT3];      // 0: nodata pixel (masking), kept out of the sums
     __shared__ float sh_aprev[kWideT3];
     __shared__ uint64_t full[kWideS3];  // bulk path: one TMA bulk copy per tile
     __shared__ float sh_par[4];
     __shared__ int sh_st;
-    __shared__ double red[kWideNT3 / 32][5];
+    __shared__ double red[NW][5];
+    __shared__ float reda[NW][32 * J];  // per-warp sum beta L' at a flush
     const long long tb = tile_begin(blockIdx.x, a.ttot, a.G), te = tile_begin(blockIdx.x + 1, a.ttot, a.G);
     const int ntl = (int)(te - tb);
     const int cfirst = (int)(tb / a.tpc);
@@ -703,28 +705,36 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
         cp_async_commit();
     }
 
-    float acc[NBT];
+    float acc[J];
 #pragma unroll
-    for (int j = 0; j < NBT; ++j) acc[j] = 0.f;
-    float sb = 0.f, sb2 = 0.f, sbs = 0.f, sbp = 0.f, swa = 0.f;
+    for (int j = 0; j < J; ++j) acc[j] = 0.f;
+    float sb = 0.f, sb2 = 0.f, sbs = 0.f, sbp = 0.f, swa = 0.f;   // lane 0 of each warp
 
     auto flush = [&](int slot) {
         double* P = a.part3 + ((size_t)blockIdx.x * a.S + slot) * (B + kPartExtra);
 #pragma unroll
-        for (int j = 0; j < NBT; ++j) {
-            const int b = tid + j * kWideNT3;
-            if (b < B) P[3 + b] = (double)acc[j];
+        for (int j = 0; j < J; ++j) {
+            reda[wid][lane + 32 * j] = acc[j];
             acc[j] = 0.f;
         }
-        float v3[5] = {sb, sb2, sbs, sbp, swa};
-#pragma unroll
-        for (int q = 0; q < 5; ++q) v3[q] = warp_sum_f(v3[q]);
-        if (lane == 0)
-            for (int q = 0; q < 5; ++q) red[wid][q] = (double)v3[q];
+        if (lane == 0) {
+            red[wid][0] = sb;
+            red[wid][1] = sb2;
+            red[wid][2] = sbs;
+            red[wid][3] = sbp;
+            red[wid][4] = swa;
+        }
         __syncthreads();
+        for (int b = tid; b < B; b += kWideNT3) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s += (double)reda[w][b];
+            P[3 + b] = s;
+        }
         if (tid < 5) {
             double s = 0.0;
-            for (int w = 0; w < kWideNT3 / 32; ++w) s += red[w][tid];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s += red[w][tid];
             P[tid < 3 ? tid : B + tid] = s;   // [0..2] and [B+3], [B+4]
         }
         __syncthreads();
@@ -734,6 +744,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
     int cur = -1;
     float mz = 0.f, cz = 0.f, q = 1.f, mmf = 1.f;
     int cst = 0;
+    float msr[J], zsr[J];   // this lane's m-hat and z entries (zero beyond B)
     TileCursor ccur(tb, a.tpc);
     for (int i = 0; i < ntl; ++i, ccur.next()) {
         const int c = ccur.c;
@@ -763,6 +774,11 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
                 if (lane == 0) sh_par[3] = s2 > 0.f ? 1.f / s2 : 0.f;
             }
             __syncthreads();
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                msr[j] = ms[lane + 32 * j];
+                zsr[j] = zs[lane + 32 * j];
+            }
             mz = sh_par[0];
             cz = sh_par[1];
             q = sh_par[2];
@@ -781,8 +797,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
         __syncthreads();        // ... and everyone's; sh_aprev visible
         int rr_;
         const float* T = buf0 + (i % kWideS3) * TF + wide_tile_shift(tile_src(tb + i, rr_));
-        // ---- phase A: a warp per PB pixels (albedo, projection, update)
-        for (int base = wid * PB; base < kWideT3; base += (kWideNT3 / 32) * PB) {
+        for (int base = wid * PB; base < rows; base += NW * PB) {
             float v[PB][J], r[PB], dz[PB];
             int bad[PB];
 #pragma unroll
@@ -792,12 +807,12 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
                 const float* row = T + (size_t)(base + pb) * B;
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
-                    // elements past the row belong to the next pixel: zero them (0 * NaN of a
-                    // neighbouring nodata pixel must not reach this one)
-                    // (without masking a non-finite neighbour makes the column NONFINITE anyway)
+                    // with masking, elements past the row belong to the next pixel: zero them
+                    // (0 * NaN of a neighbouring nodata pixel must not reach this one);
+                    // without it a non-finite neighbour makes the column NONFINITE anyway
                     const bool inrow = !MASK || lane + 32 * j < B;
                     v[pb][j] = inrow ? row[lane + 32 * j] : 0.f;
-                    r[pb] = fmaf(v[pb][j], ms[lane + 32 * j], r[pb]);
+                    r[pb] = fmaf(v[pb][j], msr[j], r[pb]);
                     if (MASK && inrow && is_nodata(v[pb][j], a.nodata)) bad[pb] = 1;
                 }
             }
@@ -809,100 +824,64 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
                 for (int pb = 0; pb < PB; ++pb) r[pb] += __shfl_xor_sync(0xffffffffu, r[pb], off);
+            float scv[PB];
 #pragma unroll
             for (int pb = 0; pb < PB; ++pb) {
-                const float sc = r[pb] * mmf;    // albedo-centred radiance L' = L - sc mhat
+                scv[pb] = r[pb] * mmf;   // albedo-centred radiance L' = L - sc mhat
                 dz[pb] = 0.f;
 #pragma unroll
-                for (int j = 0; j < J; ++j)
-                    dz[pb] = fmaf(fmaf(-sc, ms[lane + 32 * j], v[pb][j]), zs[lane + 32 * j], dz[pb]);
+                for (int j = 0; j < J; ++j) {
+                    v[pb][j] = fmaf(-scv[pb], msr[j], v[pb][j]);
+                    dz[pb] = fmaf(v[pb][j], zsr[j], dz[pb]);
+                }
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
                 for (int pb = 0; pb < PB; ++pb) dz[pb] += __shfl_xor_sync(0xffffffffu, dz[pb], off);
-            // lane pb finishes pixel base + pb
 #pragma unroll
             for (int pb = 0; pb < PB; ++pb) {
-                if (lane != pb) continue;
                 const int pp = base + pb;
-                float beta = 0.f, sc = 0.f;
-                if (pp < rows) {
-                    const size_t pix = (size_t)c * a.N + p0 + pp;
-                    if (cst != COL_OK || bad[pb]) {   // failed column or nodata pixel
+                if (pp >= rows) continue;   // warp-uniform
+                const size_t pix = (size_t)c * a.N + p0 + pp;
+                if (cst != COL_OK || bad[pb]) {   // failed column or nodata pixel
+                    if (lane == 0) {
                         a.enh[pix] = __int_as_float(0x7fc00000);
                         a.alb[pix] = __int_as_float(0x7fc00000);
-                    } else {
-                        const float r0 = r[pb];                     // albedo factor (Eq. 7)
-                        sc = r0 * mmf;
-                        const float pz = dz[pb] + fmaf(sc, mz, -cz);  // (L - mu^k).z
-                        const float rt = a.use_albedo ? fmaxf(r0, a.r_floor) : 1.f;
-                        float out;
-                        float w = 0.f;
-                        if (a.k == 0) {
-                            const float a0 = pz / (rt * q);                       // line 6
-                            out = a.n_iter == 0 ? a0 : (a0 > 0.f ? a0 : 0.f);     // reading C3
-                            a.alb[pix] = a.use_albedo ? r0 : 1.f;
-                        } else {
-                            w = a.use_sparsity ? 1.f / (sh_aprev[pp] + a.eps) : 0.f;   // Eq. 5
-                            const float x = (pz - w) / (rt * q);                      // line 16
-                            out = x > 0.f ? x : 0.f;                                  // C14
-                        }
-                        a.enh[pix] = out;
-                        beta = rt * out;
-                        if (a.energy) {
-                            sbp = fmaf(beta, pz, sbp);
-                            swa = fmaf(rt * w, fabsf(out), swa);
-                        }
                     }
+                    continue;
                 }
-                sh_bs[pp] = make_float2(beta, sc);
-                sh_ok[pp] = !bad[pb];
-                sb += beta;
-                sb2 = fmaf(beta, beta, sb2);
-                sbs = fmaf(beta, sc, sbs);
-            }
-        }
-        __syncthreads();
-        // ---- phase B: sum beta L' with a thread per band (NBT bands per thread, the
-        // (beta, sc) pair of each pixel loaded once for all of them)
-        if (accum && cst == COL_OK) {
-            float mbv[NBT];
-            const float* tcol[NBT];
+                const float r0 = r[pb];                       // albedo factor (Eq. 7)
+                const float sc = scv[pb];
+                const float pz = dz[pb] + fmaf(sc, mz, -cz);  // (L - mu^k).z
+                const float rt = a.use_albedo ? fmaxf(r0, a.r_floor) : 1.f;
+                float out;
+                float w = 0.f;
+                if (a.k == 0) {
+                    const float a0 = pz / (rt * q);                       // line 6
+                    out = a.n_iter == 0 ? a0 : (a0 > 0.f ? a0 : 0.f);     // reading C3
+                    if (lane == 0) a.alb[pix] = a.use_albedo ? r0 : 1.f;
+                } else {
+                    w = a.use_sparsity ? 1.f / (sh_aprev[pp] + a.eps) : 0.f;   // Eq. 5
+                    const float x = (pz - w) / (rt * q);                      // line 16
+                    out = x > 0.f ? x : 0.f;                                  // C14
+                }
+                const float beta = rt * out;
+                if (lane == 0) {
+                    a.enh[pix] = out;
+                    if (a.energy) {
+                        sbp = fmaf(beta, pz, sbp);
+                        swa = fmaf(rt * w, fabsf(out), swa);
+                    }
+                    sb += beta;
+                    sb2 = fmaf(beta, beta, sb2);
+                    sbs = fmaf(beta, sc, sbs);
+                }
+                if (accum) {
 #pragma unroll
-            for (int j = 0; j < NBT; ++j) {
-                const int b = tid + j * kWideNT3;
-                mbv[j] = b < B ? ms[b] : 0.f;
-                tcol[j] = T + (b < B ? b : 0);
-            }
-            float s0[NBT], s1[NBT];
-#pragma unroll
-            for (int j = 0; j < NBT; ++j) {
-                s0[j] = acc[j];
-                s1[j] = 0.f;
-            }
-            int pp = 0;
-            for (; pp + 2 <= rows; pp += 2) {
-                const float2 bs0 = sh_bs[pp], bs1 = sh_bs[pp + 1];
-                const bool ok0 = !MASK || sh_ok[pp], ok1 = !MASK || sh_ok[pp + 1];
-#pragma unroll
-                for (int j = 0; j < NBT; ++j) {
-                    const float t0 = ok0 ? tcol[j][(size_t)pp * B] : 0.f;
-                    const float t1 = ok1 ? tcol[j][(size_t)(pp + 1) * B] : 0.f;
-                    s0[j] = fmaf(bs0.x, fmaf(-bs0.y, mbv[j], t0), s0[j]);
-                    s1[j] = fmaf(bs1.x, fmaf(-bs1.y, mbv[j], t1), s1[j]);
+                    for (int j = 0; j < J; ++j) acc[j] = fmaf(beta, v[pb][j], acc[j]);
                 }
             }
-            if (pp < rows) {
-                const float2 bs0 = sh_bs[pp];
-                const bool ok0 = !MASK || sh_ok[pp];
-#pragma unroll
-                for (int j = 0; j < NBT; ++j)
-                    s0[j] = fmaf(bs0.x, fmaf(-bs0.y, mbv[j], ok0 ? tcol[j][(size_t)pp * B] : 0.f), s0[j]);
-            }
-#pragma unroll
-            for (int j = 0; j < NBT; ++j)
-                if (tid + j * kWideNT3 < B) acc[j] = s0[j] + s1[j];
         }
         fence_proxy_async();   // generic reads of slot i % S before its async-proxy refill
         __syncthreads();       // slot i % S free for tile i + S
