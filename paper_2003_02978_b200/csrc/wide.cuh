@@ -745,8 +745,21 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
     float mz = 0.f, cz = 0.f, q = 1.f, mmf = 1.f;
     int cst = 0;
     float msr[J], zsr[J];   // this lane's m-hat and z entries (zero beyond B)
+    // alpha^{k-1} of the next tile's pixels, loaded one tile ahead (threads < kWideT3) so its
+    // global-memory latency is off the per-tile critical path (Eq. 5 reweighting term)
+    const bool need_prev = a.k > 0 && a.use_sparsity;
+    TileCursor pcur(tb, a.tpc);
+    auto aprev_load = [&]() -> float {
+        const int pp = pcur.tt * kWideT3 + tid;
+        const float v = (need_prev && tid < kWideT3 && pp < a.N) ? a.enh[(size_t)pcur.c * a.N + pp] : 0.f;
+        pcur.next();
+        return v;
+    };
+    float apf = ntl > 0 ? aprev_load() : 0.f;
     TileCursor ccur(tb, a.tpc);
     for (int i = 0; i < ntl; ++i, ccur.next()) {
+        const float ap_cur = apf;
+        if (i + 1 < ntl) apf = aprev_load();
         const int c = ccur.c;
         const int p0 = ccur.tt * kWideT3;
         const int rows = min(kWideT3, a.N - p0);
@@ -786,10 +799,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             cst = sh_st;
             cur = c;
         }
-        // previous alpha of this tile's pixels (reweighting term, Eq. 5), off the critical path
-        if (tid < kWideT3)
-            sh_aprev[tid] = (a.k > 0 && a.use_sparsity && cst == COL_OK && tid < rows)
-                                ? a.enh[(size_t)c * a.N + p0 + tid] : 0.f;
+        if (tid < kWideT3) sh_aprev[tid] = ap_cur;   // (unused for failed columns / past N)
         if (a.bulk)
             mbar_wait(&full[i % kWideS3], (i / kWideS3) & 1);
         else
@@ -798,11 +808,12 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
         int rr_;
         const float* T = buf0 + (i % kWideS3) * TF + wide_tile_shift(tile_src(tb + i, rr_));
         for (int base = wid * PB; base < rows; base += NW * PB) {
-            float v[PB][J], r[PB], dz[PB];
+            float v[PB][J], r[PB], dz[PB], r2[PB], dz2[PB];   // two partial sums per dot (ILP)
             int bad[PB];
 #pragma unroll
             for (int pb = 0; pb < PB; ++pb) {
                 r[pb] = 0.f;
+                r2[pb] = 0.f;
                 bad[pb] = 0;
                 const float* row = T + (size_t)(base + pb) * B;
 #pragma unroll
@@ -812,9 +823,11 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
                     // without it a non-finite neighbour makes the column NONFINITE anyway
                     const bool inrow = !MASK || lane + 32 * j < B;
                     v[pb][j] = inrow ? row[lane + 32 * j] : 0.f;
-                    r[pb] = fmaf(v[pb][j], msr[j], r[pb]);
+                    if (j & 1) r2[pb] = fmaf(v[pb][j], msr[j], r2[pb]);
+                    else r[pb] = fmaf(v[pb][j], msr[j], r[pb]);
                     if (MASK && inrow && is_nodata(v[pb][j], a.nodata)) bad[pb] = 1;
                 }
+                r[pb] += r2[pb];
             }
             if (MASK) {
 #pragma unroll
@@ -829,11 +842,14 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             for (int pb = 0; pb < PB; ++pb) {
                 scv[pb] = r[pb] * mmf;   // albedo-centred radiance L' = L - sc mhat
                 dz[pb] = 0.f;
+                dz2[pb] = 0.f;
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
                     v[pb][j] = fmaf(-scv[pb], msr[j], v[pb][j]);
-                    dz[pb] = fmaf(v[pb][j], zsr[j], dz[pb]);
+                    if (j & 1) dz2[pb] = fmaf(v[pb][j], zsr[j], dz2[pb]);
+                    else dz[pb] = fmaf(v[pb][j], zsr[j], dz[pb]);
                 }
+                dz[pb] += dz2[pb];
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1)
