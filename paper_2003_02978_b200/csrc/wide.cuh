@@ -922,7 +922,10 @@ namespace smf {
 // epilogue into the column's fp64 partial matrix [BEp][BEp] in global memory (L2).
 // sigma_p = L_p . ghat comes from k1w_sigma (one pass, fp32, the same product order as
 // the FFMA kernels use for their own transform).
-constexpr int kRunW = 8;          // K-blocks (32 px each) per fp32 TMEM run
+#ifndef SMF_KRUNW
+#define SMF_KRUNW 8
+#endif
+constexpr int kRunW = SMF_KRUNW;  // K-blocks (32 px each) per fp32 TMEM run
 constexpr int kTW = 13 * 32;      // threads: 8 transform + 4 epilogue + 1 MMA warps
 
 struct WideTCArgs {
@@ -1067,14 +1070,34 @@ __global__ void __launch_bounds__(kTW, 1) k1w_stats_tc(WideTCArgs a) {
             mbar_wait(&acc_full[ab], (g >> 1) & 1);
             tc_fence_after();
             const uint32_t t0 = tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)(ab * 256);
+            // this thread's row: 16-column chunks, 16-byte accesses, the next chunk's old
+            // values in flight while the current one is added (latency of the L2 round trip
+            // paid about once per flush instead of once per chunk)
+            double2* prow2 = reinterpret_cast<double2*>(prow);
+            double2 cur[8], nxt[8];
+            if (!first) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) cur[k] = prow2[k];
+            }
 #pragma unroll 1
             for (int n0 = 0; n0 < 128; n0 += 16) {
+                if (!first && n0 + 16 < 128) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) nxt[k] = prow2[(n0 + 16) / 2 + k];
+                }
                 float v[16], u[16];
                 tmem_ld16x2(t0 + n0, t0 + 128 + n0, v, u);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const double s = (double)v[j] + (diag ? 2.0 : 1.0) * (double)u[j];
-                    prow[n0 + j] = first ? s : prow[n0 + j] + s;
+                for (int k = 0; k < 8; ++k) {
+                    double2 s;
+                    s.x = (double)v[2 * k] + (diag ? 2.0 : 1.0) * (double)u[2 * k];
+                    s.y = (double)v[2 * k + 1] + (diag ? 2.0 : 1.0) * (double)u[2 * k + 1];
+                    if (!first) {
+                        s.x += cur[k].x;
+                        s.y += cur[k].y;
+                    }
+                    prow2[n0 / 2 + k] = s;
+                    cur[k] = nxt[k];
                 }
             }
             tc_fence_before();

@@ -6,7 +6,8 @@ import numpy as np, torch
 from paper_2003_02978_b200 import smf, synth
 sys.path.insert(0, "/root/repo")
 import oracle
-for name, cols in (("segment", 6), ("flightline", 4)):
+cfgs = [(x.split(":")[0], int(x.split(":")[1])) for x in os.environ.get("K1ACC_CFGS", "segment:6,flightline:4").split(",")]
+for name, cols in cfgs:
     cfg = synth.scaled(synth.CONFIGS[name], cols=cols)
     cube, s, _ = synth.generate(cfg, columns=list(range(cols)))
     for k in ("tensor", "ffma"):
