@@ -624,8 +624,14 @@ __global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
 }
 
 // ---------------------------------------------------------------- K3w sweep
-constexpr int kWideT3 = 16;       // pixels per K3w tile
-constexpr int kWideS3 = 2;        // K3w cp.async ring depth (tiles in flight)
+#ifndef SMF_WT3
+#define SMF_WT3 16
+#endif
+#ifndef SMF_WS3
+#define SMF_WS3 2
+#endif
+constexpr int kWideT3 = SMF_WT3;  // pixels per K3w tile
+constexpr int kWideS3 = SMF_WS3;  // K3w ring depth (tiles in flight)
 constexpr int kWideNT3 = 128;     // threads per K3w CTA (4 warps; 4 CTAs per SM)
 
 // floats per tile buffer: 32 rows + 4 floats of alignment shift + 32 floats of zero pad
@@ -708,7 +714,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
     float acc[J];
 #pragma unroll
     for (int j = 0; j < J; ++j) acc[j] = 0.f;
-    float sb = 0.f, sb2 = 0.f, sbs = 0.f, sbp = 0.f, swa = 0.f;   // lane 0 of each warp
+    float sb = 0.f, sb2 = 0.f, sbs = 0.f, sbp = 0.f, swa = 0.f;   // lanes < PB: their pixels' sums
 
     auto flush = [&](int slot) {
         double* P = a.part3 + ((size_t)blockIdx.x * a.S + slot) * (B + kPartExtra);
@@ -717,13 +723,11 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             reda[wid][lane + 32 * j] = acc[j];
             acc[j] = 0.f;
         }
-        if (lane == 0) {
-            red[wid][0] = sb;
-            red[wid][1] = sb2;
-            red[wid][2] = sbs;
-            red[wid][3] = sbp;
-            red[wid][4] = swa;
-        }
+        float v5[5] = {sb, sb2, sbs, sbp, swa};   // nonzero in lanes < PB only
+#pragma unroll
+        for (int q5 = 0; q5 < 5; ++q5) v5[q5] = warp_sum_f(v5[q5]);
+        if (lane == 0)
+            for (int q5 = 0; q5 < 5; ++q5) red[wid][q5] = (double)v5[q5];
         __syncthreads();
         for (int b = tid; b < B; b += kWideNT3) {
             double s = 0.0;
@@ -855,47 +859,64 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
                 for (int pb = 0; pb < PB; ++pb) dz[pb] += __shfl_xor_sync(0xffffffffu, dz[pb], off);
+            // pixel tails in parallel: lane l evaluates pixel l % PB (the PB tails share one
+            // instruction stream), then beta is broadcast for the sums
+            const int myp = lane % PB;
+            float r0 = r[0], sc = scv[0], dzm = dz[0];
+            int badm = bad[0];
 #pragma unroll
-            for (int pb = 0; pb < PB; ++pb) {
-                const int pp = base + pb;
-                if (pp >= rows) continue;   // warp-uniform
-                const size_t pix = (size_t)c * a.N + p0 + pp;
-                if (cst != COL_OK || bad[pb]) {   // failed column or nodata pixel
-                    if (lane == 0) {
+            for (int pb = 1; pb < PB; ++pb)
+                if (myp == pb) {
+                    r0 = r[pb];
+                    sc = scv[pb];
+                    dzm = dz[pb];
+                    badm = bad[pb];
+                }
+            const int ppm = base + myp;
+            float beta = 0.f;
+            const bool mine = lane < PB && ppm < rows;
+            if (ppm < rows) {
+                const size_t pix = (size_t)c * a.N + p0 + ppm;
+                if (cst != COL_OK || badm) {   // failed column or nodata pixel
+                    if (mine) {
                         a.enh[pix] = __int_as_float(0x7fc00000);
                         a.alb[pix] = __int_as_float(0x7fc00000);
                     }
-                    continue;
-                }
-                const float r0 = r[pb];                       // albedo factor (Eq. 7)
-                const float sc = scv[pb];
-                const float pz = dz[pb] + fmaf(sc, mz, -cz);  // (L - mu^k).z
-                const float rt = a.use_albedo ? fmaxf(r0, a.r_floor) : 1.f;
-                float out;
-                float w = 0.f;
-                if (a.k == 0) {
-                    const float a0 = pz / (rt * q);                       // line 6
-                    out = a.n_iter == 0 ? a0 : (a0 > 0.f ? a0 : 0.f);     // reading C3
-                    if (lane == 0) a.alb[pix] = a.use_albedo ? r0 : 1.f;
                 } else {
-                    w = a.use_sparsity ? 1.f / (sh_aprev[pp] + a.eps) : 0.f;   // Eq. 5
-                    const float x = (pz - w) / (rt * q);                      // line 16
-                    out = x > 0.f ? x : 0.f;                                  // C14
-                }
-                const float beta = rt * out;
-                if (lane == 0) {
-                    a.enh[pix] = out;
-                    if (a.energy) {
-                        sbp = fmaf(beta, pz, sbp);
-                        swa = fmaf(rt * w, fabsf(out), swa);
+                    const float pz = dzm + fmaf(sc, mz, -cz);   // (L - mu^k).z
+                    const float rt = a.use_albedo ? fmaxf(r0, a.r_floor) : 1.f;
+                    float out;
+                    float w = 0.f;
+                    if (a.k == 0) {
+                        const float a0 = pz / (rt * q);                       // line 6
+                        out = a.n_iter == 0 ? a0 : (a0 > 0.f ? a0 : 0.f);     // reading C3
+                        if (mine) a.alb[pix] = a.use_albedo ? r0 : 1.f;      // Eq. 7
+                    } else {
+                        w = a.use_sparsity ? 1.f / (sh_aprev[ppm] + a.eps) : 0.f;   // Eq. 5
+                        const float x = (pz - w) / (rt * q);                       // line 16
+                        out = x > 0.f ? x : 0.f;                                   // C14
                     }
-                    sb += beta;
-                    sb2 = fmaf(beta, beta, sb2);
-                    sbs = fmaf(beta, sc, sbs);
+                    beta = rt * out;
+                    if (mine) {
+                        a.enh[pix] = out;
+                        if (a.energy) {
+                            sbp = fmaf(beta, pz, sbp);
+                            swa = fmaf(rt * w, fabsf(out), swa);
+                        }
+                        sb += beta;
+                        sb2 = fmaf(beta, beta, sb2);
+                        sbs = fmaf(beta, sc, sbs);
+                    }
                 }
-                if (accum) {
+            }
+            if (accum) {
 #pragma unroll
-                    for (int j = 0; j < J; ++j) acc[j] = fmaf(beta, v[pb][j], acc[j]);
+                for (int pb = 0; pb < PB; ++pb) {
+                    const float bp = __shfl_sync(0xffffffffu, beta, pb);   // 0 for skipped pixels
+                    if (base + pb < rows && bp != 0.f) {   // warp-uniform
+#pragma unroll
+                        for (int j = 0; j < J; ++j) acc[j] = fmaf(bp, v[pb][j], acc[j]);
+                    }
                 }
             }
         }
