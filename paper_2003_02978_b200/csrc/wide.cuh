@@ -223,7 +223,7 @@ struct WideInitArgs {
     double ridge_rel;
 };
 
-__host__ inline size_t k2w_init_smem(int B) { return (size_t)(5 * B + kGJ * kGJ + (size_t)B * (kGJ + 1) + 32 * 4) * 8; }
+__host__ inline size_t k2w_init_smem(int B) { return (size_t)(5 * B + kGJ * kGJ + (size_t)B * (kGJ + 2) + 32 * 4) * 8 + 16; }
 
 // In-place blocked Gauss-Jordan inverse of the SPD matrix A (B x B, row-major, global)
 // by one CTA: for every diagonal block K (kGJ wide), D = A_KK^-1 (shared memory,
@@ -233,8 +233,8 @@ __host__ inline size_t k2w_init_smem(int B) { return (size_t)(5 * B + kGJ * kGJ 
 // in registers. No pivoting: for an SPD matrix the pivots are the Cholesky pivots
 // squared; a pivot <= tol flags NOT_SPD.
 __device__ bool wide_gj_inverse(double* A, int B, double tol, double* D /* [kGJ][kGJ] */,
-                                double* Cp /* [B][kGJ + 1] */) {
-    constexpr int CS = kGJ + 1;
+                                double* Cp /* [B][kGJ + 2], 16-byte aligned */) {
+    constexpr int CS = kGJ + 2;   // even: rows 16-byte aligned for the double2 broadcasts
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int k0 = 0; k0 < B; k0 += kGJ) {
         const int nb = min(kGJ, B - k0);
@@ -301,12 +301,13 @@ __device__ bool wide_gj_inverse(double* A, int B, double tol, double* D /* [kGJ]
                     const int i = i0 + u;
                     if (i >= B) break;
                     if (i >= k0 && i < k0 + nb) continue;
-                    const double* ci = Cp + i * CS;
+                    const double2* ci = reinterpret_cast<const double2*>(Cp + i * CS);
                     double w0 = v[u], w1 = 0.0;
 #pragma unroll
                     for (int s2 = 0; s2 < kGJ; s2 += 2) {
-                        w0 = fma(-ci[s2], rn[s2], w0);
-                        w1 = fma(-ci[s2 + 1], rn[s2 + 1], w1);
+                        const double2 cc = ci[s2 / 2];
+                        w0 = fma(-cc.x, rn[s2], w0);
+                        w1 = fma(-cc.y, rn[s2 + 1], w1);
                     }
                     A[(size_t)i * B + j] = w0 + w1;
                 }
@@ -339,8 +340,8 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     double* vt = cv + B;         // [B] t0
     double* mh = vt + B;         // [B] fp32 mhat (as double)
     double* D = mh + B;          // [kGJ][kGJ]
-    double* Cp = D + kGJ * kGJ;        // [B][kGJ + 1] column panel
-    double* scratch = Cp + (size_t)B * (kGJ + 1);   // [32][4]
+    double* Cp = D + kGJ * kGJ + ((5 * B) & 1);   // [B][kGJ + 2] column panel (16-byte aligned)
+    double* scratch = Cp + (size_t)B * (kGJ + 2);   // [32][4]
     __shared__ int bad;
     __shared__ double sh_tol, sh_mm;
     const int BEp = a.BEp;
