@@ -1071,10 +1071,11 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
                 ProfScope ps(ctx, st, SMF_KERNEL_UPDATE);
                 if (p.wide)
                     k2w_update<<<cols, kWideNT2, smem_up, st>>>(ua);
-                else
-                {
+                else {
                     void* args[] = {(void*)&ua};
-                    launch_pdl(reinterpret_cast<const void*>(&k2_update), dim3(cols), dim3(128), args, smem_up, st);
+                    e0 = launch_pdl(reinterpret_cast<const void*>(&k2_update), dim3(cols), dim3(128), args, smem_up,
+                                    st);
+                    if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k2_update launch");
                 }
             }
             e0 = cudaGetLastError();
