@@ -16,6 +16,15 @@ Parity status per function:
   closed-form MF (P2), invariants (P3), exact recovery on a noiseless scene (P4)
   and the numpy transcription (P5) (tests/test_oracle_pins.py). Its absolute
   maps on noisy scenes beyond those pins are "parity unpinned".
+  oracle_energy / the energy trace (Eq. 8, reading C19) -- pinned by E = N*B at
+  alpha = 0, E = penalty at an exact fit, a direct per-pixel sum and the trace
+  wiring (tests/test_oracle_steps.py).
+  retrieve_masked (reading C22) -- the valid rows retrieved as a column of their own,
+  pinned bitwise against retrieve_column on the filtered rows, NaN fill and the
+  INSUFFICIENT status (tests/test_oracle_pins.py).
+  Detector grouping (reading C20) has no function of its own: a partition of G
+  columns is retrieve_column on their pooled pixels (pixel-permutation invariance,
+  P3, pins the pooling order).
 """
 from __future__ import annotations
 

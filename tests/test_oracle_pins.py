@@ -333,3 +333,29 @@ def test_p6_energy_converges(oracle_lib):
     E = dg["energy"]
     assert rc == 0 and np.isfinite(E).all()
     assert abs(E[30] - E[20]) <= 0.01 * abs(E[30])
+
+
+# ---------------------------------------------------------------- masking (reading C22)
+def test_masked_retrieval_is_retrieval_of_the_valid_rows(oracle_lib):
+    """Nodata masking (P:545 censored regions, DESIGN reading C22): a pixel with any band
+    non-finite or equal to the nodata value takes no part; the remaining rows are retrieved
+    exactly as a column of their own (bitwise), masked pixels read NaN, and a column left
+    with < 2 valid rows reports INSUFFICIENT (5) with all-NaN maps."""
+    rng = np.random.default_rng(77)
+    L, s = _random_instance(rng, 60, 9)
+    nodata = np.float32(-9999.0)
+    cube = np.stack([L.copy(), L.copy(), L[:3].repeat(20, axis=0)])
+    bad = [3, 17, 40]
+    cube[0, bad[0], 2] = nodata          # one band equal to nodata
+    cube[0, bad[1], 0] = np.nan          # non-finite bands
+    cube[0, bad[2], 8] = np.inf
+    cube[2, 1:, 4] = nodata              # column 2: one valid row left
+    alpha, r, st = oracle_lib.retrieve_masked(cube, s, nodata, n_iter=6)
+    keep = np.setdiff1d(np.arange(60), bad)
+    a0, r0, rc0 = oracle_lib.retrieve_column(L[keep], s, n_iter=6)
+    assert st[0] == rc0 == 0
+    assert np.array_equal(alpha[0, keep], a0) and np.array_equal(r[0, keep], r0)
+    assert np.all(np.isnan(alpha[0, bad])) and np.all(np.isnan(r[0, bad]))
+    a1, r1, _ = oracle_lib.retrieve_column(L, s, n_iter=6)   # nothing masked: plain retrieval
+    assert st[1] == 0 and np.array_equal(alpha[1], a1) and np.array_equal(r[1], r1)
+    assert st[2] == 5 and np.all(np.isnan(alpha[2])) and np.all(np.isnan(r[2]))
