@@ -139,6 +139,12 @@ smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols,
                              float* enhancement_host, float* albedo_host,
                              int32_t* column_status_host);
 
+/* Columns per chunk that smf_retrieve_host uses for a cube of `cols` columns with
+ * this context's grouping (whole detector groups per chunk; ~24 chunks, at most
+ * cols/16; the last chunk may be shorter). Writes *chunk_cols; SMF_ERR_INVALID_ARGUMENT for a
+ * NULL pointer or cols < 1. */
+smf_status smf_host_chunk_cols(const smf_ctx* ctx, int cols, int* chunk_cols);
+
 /* Per-column background model after the last smf_retrieve that used
  * `workspace`: mu^{N_iter} (device fp64 [cols][bands], or NULL) and
  * q^{N_iter} = t^T (C+rho I)^-1 t (device fp64 [cols], or NULL). Enqueued on

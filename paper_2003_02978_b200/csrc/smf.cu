@@ -397,6 +397,21 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_
     return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
+// smf_retrieve_host chunking: ~24 chunks of whole detector groups -- the exposed tail
+// (the last chunk's retrieval and download) shrinks with the chunk while every chunk's
+// retrieval still hides under the next upload (SMF_HOST_CHUNKS overrides the target).
+int host_chunk_cols(int group, int cols) {
+    static const int target = [] {
+        const char* e = std::getenv("SMF_HOST_CHUNKS");
+        const int v = e ? std::atoi(e) : 24;
+        return v > 0 ? v : 24;
+    }();
+    const int G = std::max(1, std::min(group, cols));
+    const int ngroups = (cols + G - 1) / G;
+    const int want = std::max(1, std::min(target, cols / 16));
+    return (ngroups + want - 1) / want * G;
+}
+
 // Serpentine sweep order (narrow path): alternate sweeps walk each CTA's tile range
 // backwards so the start of a pass hits the L2-resident tail of the previous one.
 // SMF_SERPENTINE=0 turns it off (A/B measurement).
@@ -1143,6 +1158,12 @@ smf_status smf_synchronize(smf_ctx* ctx, void* stream, const int32_t* column_sta
     return SMF_OK;
 }
 
+smf_status smf_host_chunk_cols(const smf_ctx* ctx, int cols, int* chunk_cols) {
+    if (!ctx || !chunk_cols || cols < 1) return SMF_ERR_INVALID_ARGUMENT;
+    *chunk_cols = host_chunk_cols(ctx->group, cols);
+    return SMF_OK;
+}
+
 smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols, int pixels,
                              float* enhancement_host, float* albedo_host, int32_t* column_status_host) {
     // Columns are independent partitions, so the cube is streamed in column
@@ -1158,10 +1179,8 @@ smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols,
         for (int k = 0; k < 6 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&ctx->h_ev[k], cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "stream create");
     }
-    const int G = std::min(ctx->group, cols);   // chunks hold whole detector groups
-    const int ngroups = (cols + G - 1) / G;
-    const int nchunks = std::max(1, std::min(std::min(8, cols / 64), ngroups));
-    const int ccols = (ngroups + nchunks - 1) / nchunks * G;   // columns per chunk (last may be short)
+    const int ccols = host_chunk_cols(ctx->group, cols);   // whole detector groups (last may be short)
+    const int nchunks = (cols + ccols - 1) / ccols;           // every chunk non-empty
     size_t ws_bytes = 0, ws_last = 0;
     smf_workspace_bytes(ctx, ccols, pixels, &ws_bytes);
     smf_workspace_bytes(ctx, cols - (nchunks - 1) * ccols > 0 ? cols - (nchunks - 1) * ccols : ccols, pixels,

@@ -47,6 +47,7 @@ SYMBOLS = {
     "smf_group_partitions": (_i, [_i, _i, ctypes.POINTER(_i), ctypes.POINTER(_i)]),
     "smf_energy_trace": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "smf_stats_kernel_used": (_i, [_vp]),
+    "smf_host_chunk_cols": (_i, [_vp, _i, ctypes.POINTER(_i)]),
     "smf_profile_enable": (_i, [_vp, _i]),
     "smf_profile_read": (_i, [_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_i)]),
     "smf_status_string": (ctypes.c_char_p, [_i]),
@@ -246,6 +247,12 @@ class Retriever:
         if rc not in (SMF_OK, SMF_ERR_NUMERICAL):
             self._check(rc)
         return enhancement, albedo, status, rc
+
+    def host_chunk_cols(self, cols: int) -> int:
+        """Columns per chunk that retrieve_host streams for a cube of `cols` columns."""
+        n = _i()
+        self._check(_lib.smf_host_chunk_cols(self._h, int(cols), ctypes.byref(n)))
+        return n.value
 
     def retrieve_host_ptr(self, rad_ptr, cols, pixels, enh_ptr, alb_ptr, status_ptr):
         """Same as retrieve_host on raw host pointers (e.g. pinned torch tensors)."""

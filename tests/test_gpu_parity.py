@@ -371,7 +371,7 @@ def test_determinism_and_host_path(smf, torch):
 
 
 def test_host_path_chunked(smf, torch):
-    """smf_retrieve_host streams column chunks (3 here) through two device slots with
+    """smf_retrieve_host streams column chunks (12 here) through two device slots with
     overlapped copies. Each chunk equals a device-resident retrieval of the same columns
     bit for bit; against the whole-cube launch only the per-column reduction order (the
     CTA partition) differs, so that comparison uses the C18 bar."""
@@ -380,7 +380,8 @@ def test_host_path_chunked(smf, torch):
     r = smf.Retriever(cfg.bands, s, n_iter=30)
     eh, ah, sh, rc = r.retrieve_host(cube)
     assert rc == 0 and (sh == 0).all()
-    chunk = 67   # 200 columns -> 3 chunks of ceil(200/3)
+    chunk = r.host_chunk_cols(200)
+    assert chunk == 17   # 200 columns -> 12 chunks (target 24, at most cols/16)
     for c0 in range(0, 200, chunk):
         ec, ac, stc, *_ = run_gpu(smf, torch, cube[c0:c0 + chunk], s, n_iter=30)
         np.testing.assert_array_equal(eh[c0:c0 + chunk], ec)
