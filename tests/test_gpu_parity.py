@@ -174,7 +174,7 @@ def test_ragged_shapes(smf, torch, cols, pixels, bands):
 
 # ------------------------------------------------------------------ wide path (any band count)
 @pytest.mark.parametrize("cols,pixels,bands", [(2, 300, 5), (3, 257, 13), (2, 700, 101), (1, 130, 98),
-                                               (2, 1200, 425)])
+                                               (2, 1200, 425), (2, 200, 1), (2, 200, 2), (1, 3000, 626)])
 def test_wide_bands(smf, torch, cols, pixels, bands):
     """Band counts outside the narrow kernels (B % 4 != 0 or B > 96) run the wide path
     (k1w_stats / k2w_init / k2w_update / k3w_sweep)."""
