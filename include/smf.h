@@ -123,6 +123,15 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
                         float* enhancement, float* albedo, void* workspace,
                         int32_t* column_status, void* stream);
 
+/* CUDA-graph mode (enable != 0; default off): smf_retrieve captures its launch
+ * sequence (statistics, factorisation, N_iter + 1 sweeps and updates) into a CUDA
+ * graph on the first call and replays it with one cudaGraphLaunch while the call's
+ * pointers, shape and stream and the context's settings (every smf_set_* call
+ * invalidates it) are unchanged; results are bitwise those of the eager launches.
+ * Calls on the legacy default stream (stream == NULL) and calls with profiling on
+ * run eagerly. smf_retrieve_host always runs eagerly. */
+smf_status smf_set_graph(smf_ctx* ctx, int enable);
+
 /* Wait for `stream`, then read `column_status` (device int32 [cols], as passed
  * to smf_retrieve) and report the first failed column (-1 if none).
  * Returns SMF_ERR_NUMERICAL if any column failed, SMF_ERR_CUDA on a CUDA error. */

@@ -50,6 +50,20 @@ struct smf_ctx {
     cudaEvent_t h_ev[8] = {};          // [0,2) uploaded, [2,4) computed, [4,6) downloaded
     void* h_buf = nullptr;
     size_t h_buf_bytes = 0;
+    // CUDA-graph mode (smf_set_graph): the launch sequence of the last smf_retrieve,
+    // captured once and replayed while the call's arguments and settings are unchanged
+    int graph = 0;
+    unsigned gen = 0;                  // bumped by every setter: invalidates the graph
+    cudaGraphExec_t gexec = nullptr;
+    struct GKey {
+        const void* rad; int cols, pixels; const void* enh; const void* alb; const void* ws;
+        const void* status; const void* stream; unsigned gen;
+        bool operator==(const GKey& o) const {
+            return rad == o.rad && cols == o.cols && pixels == o.pixels && enh == o.enh && alb == o.alb &&
+                   ws == o.ws && status == o.status && stream == o.stream && gen == o.gen;
+        }
+    } gkey = {};
+    int glaunches = 0;
 };
 
 namespace {
@@ -827,11 +841,13 @@ void smf_destroy(smf_ctx* ctx) {
     if (ctx->h_down) cudaStreamDestroy(ctx->h_down);
     for (auto ev : ctx->h_ev)
         if (ev) cudaEventDestroy(ev);
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     delete ctx;
 }
 
 smf_status smf_set_absorption(smf_ctx* ctx, const float* s_host, int bands) {
     if (!ctx || !s_host) return SMF_ERR_INVALID_ARGUMENT;
+    ++ctx->gen;
     if (bands != ctx->bands) {
         set_err(ctx, "bands %d != context bands %d", bands, ctx->bands);
         return SMF_ERR_SHAPE;
@@ -844,6 +860,7 @@ smf_status smf_set_absorption(smf_ctx* ctx, const float* s_host, int bands) {
 
 smf_status smf_set_regularisation(smf_ctx* ctx, double epsilon, double ridge_rel, double r_floor) {
     if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    ++ctx->gen;
     if (!(epsilon > 0.0) || !(ridge_rel >= 0.0) || !(r_floor > 0.0)) {
         set_err(ctx, "need epsilon > 0, ridge_rel >= 0, r_floor > 0");
         return SMF_ERR_INVALID_ARGUMENT;
@@ -856,6 +873,7 @@ smf_status smf_set_regularisation(smf_ctx* ctx, double epsilon, double ridge_rel
 
 smf_status smf_set_iterations(smf_ctx* ctx, int n_iter, int use_sparsity, int use_albedo) {
     if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    ++ctx->gen;
     if (n_iter < 0) {
         set_err(ctx, "n_iter < 0");
         return SMF_ERR_INVALID_ARGUMENT;
@@ -868,6 +886,7 @@ smf_status smf_set_iterations(smf_ctx* ctx, int n_iter, int use_sparsity, int us
 
 smf_status smf_set_nodata(smf_ctx* ctx, int enable, float value) {
     if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    ++ctx->gen;
     ctx->mask = enable ? 1 : 0;
     ctx->nodata = value;
     return SMF_OK;
@@ -875,6 +894,7 @@ smf_status smf_set_nodata(smf_ctx* ctx, int enable, float value) {
 
 smf_status smf_set_energy_trace(smf_ctx* ctx, int enable) {
     if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    ++ctx->gen;
     ctx->energy = enable ? 1 : 0;
     return SMF_OK;
 }
@@ -916,6 +936,7 @@ smf_status smf_energy_trace(smf_ctx* ctx, const void* workspace, int cols, int p
 
 smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind) {
     if (!ctx || kind < SMF_STATS_AUTO || kind > SMF_STATS_TENSOR) return SMF_ERR_INVALID_ARGUMENT;
+    ++ctx->gen;
     if (kind == SMF_STATS_TENSOR && narrow(ctx->bands) && !k1tc_fits(ctx->bands)) {
         set_err(ctx, "tensor-core statistics kernel unavailable for %d bands", ctx->bands);
         return SMF_ERR_SHAPE;
@@ -958,6 +979,7 @@ smf_status smf_group_partitions(int cols, int group, int* n_partitions, int* fir
 
 smf_status smf_set_grouping(smf_ctx* ctx, int group) {
     if (!ctx || group < 1) return SMF_ERR_INVALID_ARGUMENT;
+    ++ctx->gen;
     ctx->group = group;
     return SMF_OK;
 }
@@ -975,8 +997,8 @@ smf_status smf_workspace_bytes(const smf_ctx* ctx, int cols, int pixels, size_t*
     return SMF_OK;
 }
 
-smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixels, float* enhancement,
-                        float* albedo, void* workspace, int32_t* column_status, void* stream) {
+static smf_status retrieve_eager(smf_ctx* ctx, const float* radiance, int cols, int pixels, float* enhancement,
+                                 float* albedo, void* workspace, int32_t* column_status, void* stream) {
     if (ctx && ctx->group > 1 && cols >= 1) {
         // detector grouping: the full groups are one retrieval over nfull partitions of
         // G * pixels rows (the G columns of a group are contiguous in [cols][pixels][bands]),
@@ -989,12 +1011,12 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
             int32_t* pst = (int32_t*)(ws + g.o_status);
             const int saved = ctx->group;
             ctx->group = 1;
-            smf_status rc = smf_retrieve(ctx, radiance, g.nfull, g.G * pixels, enhancement, albedo,
+            smf_status rc = retrieve_eager(ctx, radiance, g.nfull, g.G * pixels, enhancement, albedo,
                                          ws + g.o_full, pst, stream);
             int launches = ctx->last_launches;
             if (rc == SMF_OK && g.rem > 0) {
                 const size_t off = (size_t)g.nfull * g.G * pixels;
-                rc = smf_retrieve(ctx, radiance + off * ctx->bands, 1, g.rem * pixels, enhancement + off,
+                rc = retrieve_eager(ctx, radiance + off * ctx->bands, 1, g.rem * pixels, enhancement + off,
                                   albedo + off, ws + g.o_rem, pst + g.nfull, stream);
                 launches += ctx->last_launches;
             }
@@ -1132,6 +1154,54 @@ smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixel
     return SMF_OK;
 }
 
+smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixels, float* enhancement,
+                        float* albedo, void* workspace, int32_t* column_status, void* stream) {
+    if (!ctx || !ctx->graph || ctx->prof || !stream)   // (the legacy stream cannot be captured)
+        return retrieve_eager(ctx, radiance, cols, pixels, enhancement, albedo, workspace, column_status, stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    const smf_ctx::GKey key = {radiance, cols, pixels, enhancement, albedo, workspace, column_status, stream,
+                               ctx->gen};
+    if (!(ctx->gexec && key == ctx->gkey)) {
+        if (ctx->gexec) {
+            cudaGraphExecDestroy(ctx->gexec);
+            ctx->gexec = nullptr;
+        }
+        cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "graph capture begin");
+        smf_status rc = retrieve_eager(ctx, radiance, cols, pixels, enhancement, albedo, workspace, column_status,
+                                       stream);
+        cudaGraph_t graph = nullptr;
+        e = cudaStreamEndCapture(st, &graph);
+        if (rc != SMF_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "graph capture end");
+        e = cudaGraphInstantiate(&ctx->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            ctx->gexec = nullptr;
+            return cuda_fail(ctx, e, "graph instantiate");
+        }
+        ctx->gkey = key;
+        ctx->glaunches = ctx->last_launches;
+    }
+    cudaError_t e = cudaGraphLaunch(ctx->gexec, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "graph launch");
+    ctx->last_launches = ctx->glaunches;
+    return SMF_OK;
+}
+
+smf_status smf_set_graph(smf_ctx* ctx, int enable) {
+    if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    ctx->graph = enable ? 1 : 0;
+    if (!ctx->graph && ctx->gexec) {
+        cudaGraphExecDestroy(ctx->gexec);
+        ctx->gexec = nullptr;
+    }
+    return SMF_OK;
+}
+
 smf_status smf_synchronize(smf_ctx* ctx, void* stream, const int32_t* column_status, int cols,
                            int* first_failed_column) {
     if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
@@ -1226,7 +1296,7 @@ smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols,
         if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->h_stream, up[k], 0);
         if (e == cudaSuccess && i >= 2) e = cudaStreamWaitEvent(ctx->h_stream, down[k], 0);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "retrieve_host upload");
-        smf_status rc = smf_retrieve(ctx, d_rad[k], nc, pixels, d_enh[k], d_alb[k], d_ws, d_st + c0, ctx->h_stream);
+        smf_status rc = retrieve_eager(ctx, d_rad[k], nc, pixels, d_enh[k], d_alb[k], d_ws, d_st + c0, ctx->h_stream);
         if (rc != SMF_OK) return rc;
         launches += ctx->last_launches;
         e = cudaEventRecord(done[k], ctx->h_stream);

@@ -48,6 +48,7 @@ SYMBOLS = {
     "smf_energy_trace": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "smf_stats_kernel_used": (_i, [_vp]),
     "smf_host_chunk_cols": (_i, [_vp, _i, ctypes.POINTER(_i)]),
+    "smf_set_graph": (_i, [_vp, _i]),
     "smf_profile_enable": (_i, [_vp, _i]),
     "smf_profile_read": (_i, [_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_i)]),
     "smf_status_string": (ctypes.c_char_p, [_i]),
@@ -118,7 +119,7 @@ class Retriever:
     STATS_KERNELS = {"auto": 0, "ffma": 1, "tensor": 2}
 
     def __init__(self, bands, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2, ridge_rel=0.0,
-                 r_floor=0.05, stats_kernel="auto", energy=False, group=1, nodata=None):
+                 r_floor=0.05, stats_kernel="auto", energy=False, group=1, nodata=None, graph=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("smf needs a CUDA device (no CPU fallback)")
@@ -135,6 +136,7 @@ class Retriever:
         self._check(_lib.smf_set_grouping(self._h, int(group)))
         self._check(_lib.smf_set_nodata(self._h, int(nodata is not None),
                                         float(nodata) if nodata is not None else -9999.0))
+        self._check(_lib.smf_set_graph(self._h, int(bool(graph))))
         self.group = int(group)
         self.n_iter = int(n_iter)
 

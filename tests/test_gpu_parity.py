@@ -409,3 +409,34 @@ def test_r_floor_pixel(smf, torch):
     a_ref, r_ref, _ = oracle.retrieve(cube, s, n_iter=6)
     assert alb[0, 5] < 0
     print(assert_parity(enh, alb, a_ref, r_ref, "r_floor"))
+
+
+def test_graph_mode_is_bitwise_eager(smf, torch):
+    """smf_set_graph: the captured launch sequence replays bitwise the eager results; a
+    setter call (smf_set_iterations) invalidates the graph and the re-capture follows it."""
+    cfg = synth.scaled(synth.CONFIGS["segment"], cols=12, pixels=1500)
+    cube, s, _ = synth.generate(cfg)
+    rad = torch.from_numpy(cube).cuda()
+    e_ref, a_ref, *_ = run_gpu(smf, torch, cube, s, n_iter=30)
+    e5, a5, *_ = run_gpu(smf, torch, cube, s, n_iter=5)
+    side = torch.cuda.Stream()
+    r = smf.Retriever(cfg.bands, s, n_iter=30, graph=True)
+    ws = r.alloc_workspace(cfg.cols, cfg.pixels)
+    enh = torch.empty((cfg.cols, cfg.pixels), device="cuda")
+    alb = torch.empty_like(enh)
+    st = torch.empty(cfg.cols, dtype=torch.int32, device="cuda")
+    for _ in range(3):   # capture, then two replays
+        enh.fill_(-1.0)
+        alb.fill_(-1.0)
+        with torch.cuda.stream(side):
+            r.retrieve(rad, enh, alb, ws, st, stream=side)
+        side.synchronize()
+        assert r.last_launch_count > 60
+        np.testing.assert_array_equal(enh.cpu().numpy(), e_ref)
+        np.testing.assert_array_equal(alb.cpu().numpy(), a_ref)
+    smf._lib.smf_set_iterations(r._h, 5, 1, 1)
+    with torch.cuda.stream(side):
+        r.retrieve(rad, enh, alb, ws, st, stream=side)
+    side.synchronize()
+    np.testing.assert_array_equal(enh.cpu().numpy(), e5)
+    np.testing.assert_array_equal(alb.cpu().numpy(), a5)
