@@ -1,0 +1,33 @@
+"""Per-tile event timeline of K1-TC CTA 0 from a trace build (debug aid; VARIANT_ROOT must
+point at a build with the K1TR instrumentation and smf_debug_k1_trace)."""
+import os, sys, ctypes
+sys.path.insert(0, os.environ["VARIANT_ROOT"])
+import numpy as np, torch
+from paper_2003_02978_b200 import smf, synth
+cfg = synth.CONFIGS["flightline"]
+cube = torch.empty((cfg.cols, cfg.pixels, cfg.bands), dtype=torch.float32, device="cuda").uniform_(0.5, 1.5)
+s = (-np.abs(np.random.default_rng(0).standard_normal(cfg.bands)) * 1e-5).astype(np.float32)
+r = smf.Retriever(cfg.bands, s, stats_kernel="tensor")
+ws = r.alloc_workspace(cfg.cols, cfg.pixels)
+for _ in range(3): r.initial_statistics(cube, workspace=ws)
+torch.cuda.synchronize()
+buf = np.zeros(8 * 4096, dtype=np.uint64)
+smf._lib.smf_debug_k1_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+assert smf._lib.smf_debug_k1_trace(buf.ctypes.data, 8 * 4096) == 0
+t = buf.reshape(8, 4096).astype(np.int64)
+n = int((t[3] > 0).sum())
+t = t[:, :n] - t[5, 0]
+names = ["raw_ready", "op_free", "op_done", "mma_start", "mma_issued", "tma_issue", "epi_start", "epi_done"]
+print("tiles", n, "total cycles", t[4, n - 1])
+for k in range(8):
+    v = t[k][t[k] != -t[5, 0]] if k >= 6 else t[k]
+print("per-tile intervals (median cycles):")
+mid = slice(20, n - 20)
+d = lambda a, b: np.median((t[b] - t[a])[mid])
+print(" tile period (mma_start[i+1]-mma_start[i])", np.median(np.diff(t[3])[20:n - 20]))
+print(" transform: raw_ready->op_free", d(0, 1), " op_free->op_done", d(1, 2))
+print(" op_done->mma_start", d(2, 3), " mma_start->mma_issued", d(3, 4))
+print(" tma_issue->raw_ready", d(5, 0))
+print(" group period (raw_ready[i+2]-raw_ready[i])", np.median((t[0][2:] - t[0][:-2])[20:n - 20]))
+ep = t[6][t[6] != 0]
+print(" first 12 tiles:\n", t[:, :12].T)
