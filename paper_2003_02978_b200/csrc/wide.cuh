@@ -1035,40 +1035,49 @@ __global__ void __launch_bounds__(kTW, 1) k1w_stats_tc(WideTCArgs a) {
         const uint32_t ops0 = smem_u32(ops);
         const uint32_t rowH = (uint32_t)(half ? 256 + r : r) * 128, rowL = rowH + 128 * 128;
         const uint32_t sw = (uint32_t)(r & 7);
-        for (int kb = 0; kb < nkb; ++kb) {
+        // Register double buffer (measured: one K-block's loads took ~2000 of its ~3000
+        // cycles when issued after the previous K-block was published): the 32 radiance
+        // values of K-block kb + 1 and lane j's sigma of pixel p0 + j are in flight while
+        // K-block kb is transformed; sigma is broadcast with shuffles.
+        const int bl = b < B ? b : B - 1;
+        const bool all_bands = __all_sync(0xffffffffu, b < B);   // no extended-row entry in this warp
+        auto load = [&](int kb, float (&lv)[32], float& sl) {
+            const int p0 = kb * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) lv[j] = __ldg(Lc + (size_t)min(p0 + j, N - 1) * B + bl);
+            sl = __ldg(sg + min(p0 + lane, N - 1));
+        };
+        auto process = [&](int kb, float (&lv)[32], const float sl) {
             const int s2 = kb & 1;
             if (kb >= 2) mbar_wait(&op_empty[s2], ((kb >> 1) - 1) & 1);
             if (work) {
                 const int p0 = kb * 32;
-                // all 64 loads issued before any use (clamped addresses, no branches), then
-                // the extended-row entry selected per band kind
-                float lv[32], sv[32];
-                const int bl = b < B ? b : B - 1;
+                // the extended-row entry selected per band kind (in place); the common case
+                // (a band row, a full K-block, no masking) is one shuffle and one FFMA
+                if (all_bands && p0 + 32 <= N && !a.mask) {   // warp-uniform (shuffles below)
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int p = min(p0 + j, N - 1);
-                    lv[j] = __ldg(Lc + (size_t)p * B + bl);
-                    sv[j] = __ldg(sg + p);
-                }
-                float x[32];
+                    for (int j = 0; j < 32; ++j) lv[j] = fmaf(-__shfl_sync(0xffffffffu, sl, j), cb, lv[j]);
+                } else {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float xb = fmaf(-sv[j], cb, lv[j]);
-                    const float v = b < B ? xb : (b == B ? sv[j] - 1.f : (b == B + 1 ? 1.f : 0.f));
-                    x[j] = (p0 + j < N && !(a.mask && isnan(sv[j]))) ? v : 0.f;
+                    for (int j = 0; j < 32; ++j) {
+                        const float sv = __shfl_sync(0xffffffffu, sl, j);
+                        const float xb = fmaf(-sv, cb, lv[j]);
+                        const float v = b < B ? xb : (b == B ? sv - 1.f : (b == B + 1 ? 1.f : 0.f));
+                        lv[j] = (p0 + j < N && !(a.mask && isnan(sv))) ? v : 0.f;
+                    }
                 }
                 const uint32_t base = ops0 + s2 * STAGE;
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     float4 h, l;
-                    h.x = tf32_rna(x[4 * q + 0]);
-                    h.y = tf32_rna(x[4 * q + 1]);
-                    h.z = tf32_rna(x[4 * q + 2]);
-                    h.w = tf32_rna(x[4 * q + 3]);
-                    l.x = x[4 * q + 0] - h.x;
-                    l.y = x[4 * q + 1] - h.y;
-                    l.z = x[4 * q + 2] - h.z;
-                    l.w = x[4 * q + 3] - h.w;
+                    h.x = tf32_rna(lv[4 * q + 0]);
+                    h.y = tf32_rna(lv[4 * q + 1]);
+                    h.z = tf32_rna(lv[4 * q + 2]);
+                    h.w = tf32_rna(lv[4 * q + 3]);
+                    l.x = lv[4 * q + 0] - h.x;
+                    l.y = lv[4 * q + 1] - h.y;
+                    l.z = lv[4 * q + 2] - h.z;
+                    l.w = lv[4 * q + 3] - h.w;
                     const uint32_t off = (((uint32_t)q ^ sw) << 4);
                     sts4(base + rowH + off, h);
                     sts4(base + rowL + off, l);
@@ -1077,6 +1086,16 @@ __global__ void __launch_bounds__(kTW, 1) k1w_stats_tc(WideTCArgs a) {
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&op_full[s2]);
+        };
+        float la[32], lb[32], sa = 0.f, sb = 0.f;
+        if (work) load(0, la, sa);
+        for (int kb = 0; kb < nkb; kb += 2) {
+            if (work && kb + 1 < nkb) load(kb + 1, lb, sb);
+            process(kb, la, sa);
+            if (kb + 1 < nkb) {
+                if (work && kb + 2 < nkb) load(kb + 2, la, sa);
+                process(kb + 1, lb, sb);
+            }
         }
     } else if (wid < 12) {
         // ===================== epilogue: TMEM -> fp64 partial (global) =====================
