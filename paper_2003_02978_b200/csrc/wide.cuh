@@ -945,7 +945,7 @@ namespace smf {
 // sigma_p = L_p . ghat comes from k1w_sigma (one pass, fp32, the same product order as
 // the FFMA kernels use for their own transform).
 #ifndef SMF_KRUNW
-#define SMF_KRUNW 8
+#define SMF_KRUNW 16
 #endif
 constexpr int kRunW = SMF_KRUNW;  // K-blocks (32 px each) per fp32 TMEM run
 constexpr int kTW = 13 * 32;      // threads: 8 transform + 4 epilogue + 1 MMA warps
