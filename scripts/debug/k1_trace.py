@@ -17,17 +17,11 @@ assert smf._lib.smf_debug_k1_trace(buf.ctypes.data, 8 * 4096) == 0
 t = buf.reshape(8, 4096).astype(np.int64)
 n = int((t[3] > 0).sum())
 t = t[:, :n] - t[5, 0]
-names = ["raw_ready", "op_free", "op_done", "mma_start", "mma_issued", "tma_issue", "epi_start", "epi_done"]
-print("tiles", n, "total cycles", t[4, n - 1])
-for k in range(8):
-    v = t[k][t[k] != -t[5, 0]] if k >= 6 else t[k]
-print("per-tile intervals (median cycles):")
+names = ["raw_ready", "sigma_done", "op_free", "stores_issued", "published", "mma_start", "mma_issued", "tma_issue"]
+print("tiles", n)
 mid = slice(20, n - 20)
-d = lambda a, b: np.median((t[b] - t[a])[mid])
-print(" tile period (mma_start[i+1]-mma_start[i])", np.median(np.diff(t[3])[20:n - 20]))
-print(" transform: raw_ready->op_free", d(0, 1), " op_free->op_done", d(1, 2))
-print(" op_done->mma_start", d(2, 3), " mma_start->mma_issued", d(3, 4))
-print(" tma_issue->raw_ready", d(5, 0))
-print(" group period (raw_ready[i+2]-raw_ready[i])", np.median((t[0][2:] - t[0][:-2])[20:n - 20]))
-ep = t[6][t[6] != 0]
-print(" first 12 tiles:\n", t[:, :12].T)
+d = lambda a, b: float(np.median((t[b] - t[a])[mid]))
+print(" tile period (mma_start)", float(np.median(np.diff(t[5])[20:n - 20])))
+print(" group: raw->sigma", d(0, 1), " sigma->opfree", d(1, 2), " opfree->stores", d(2, 3), " stores->published", d(3, 4))
+print(" published->mma_start", d(4, 5), " mma_start->issued", d(5, 6), " tma_issue->raw_ready", d(7, 0))
+print(" group period (raw_ready[i+2]-raw_ready[i])", float(np.median((t[0][2:] - t[0][:-2])[20:n - 20])))
