@@ -567,6 +567,7 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
                         ((kch ^ (uint32_t)jj ^ (uint32_t)((4 * q0) & 7)) << 4);
         TileCursor cur(tb + grp, a.tpc);
         int ccol = -1;
+        float4 pq[K::HQ];   // this thread's pilot quads, in registers (refreshed per column)
         for (int i = grp; i < ntl; i += 2) {
             const int c = cur.c, row0 = cur.tt * kTileTC;
             cur.next();
@@ -578,6 +579,9 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
                     gh[wid][b] = a.ghat32[(size_t)c * a.B + b];
                 }
                 __syncwarp();
+#pragma unroll
+                for (int q = 0; q < K::HQ; ++q)
+                    pq[q] = *reinterpret_cast<const float4*>(&pil[wid][4 * (q0 + q < NQ ? q0 + q : NQ - 1)]);
                 ccol = c;
             }
             const int s = i % K::RS, o = i % kOpStagesTC;
@@ -626,7 +630,7 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
                 if (q >= nqp) break;
                 float xs[4];
                 if (qq < NQ) {
-                    const float4 cq = *reinterpret_cast<const float4*>(&pil[wid][4 * qq]);
+                    const float4 cq = pq[q];
                     xs[0] = use ? fmaf(-sg, cq.x, v[q].x) : 0.f;
                     xs[1] = use ? fmaf(-sg, cq.y, v[q].y) : 0.f;
                     xs[2] = use ? fmaf(-sg, cq.z, v[q].z) : 0.f;
