@@ -11,10 +11,11 @@ r = smf.Retriever(cfg.bands, s, stats_kernel="tensor")
 ws = r.alloc_workspace(cfg.cols, cfg.pixels)
 for _ in range(3): r.initial_statistics(cube, workspace=ws)
 torch.cuda.synchronize()
-buf = np.zeros(8 * 4096, dtype=np.uint64)
+buf = np.zeros(10 * 4096, dtype=np.uint64)
 smf._lib.smf_debug_k1_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
-assert smf._lib.smf_debug_k1_trace(buf.ctypes.data, 8 * 4096) == 0
-t = buf.reshape(8, 4096).astype(np.int64)
+assert smf._lib.smf_debug_k1_trace(buf.ctypes.data, 10 * 4096) == 0
+t = buf.reshape(10, 4096).astype(np.int64)
+flush_mask = t[8] > 0
 n = int((t[3] > 0).sum())
 t = t[:, :n] - t[5, 0]
 names = ["raw_ready", "sigma_done", "op_free", "stores_issued", "published", "mma_start", "mma_issued", "tma_issue"]
@@ -25,3 +26,9 @@ print(" tile period (mma_start)", float(np.median(np.diff(t[5])[20:n - 20])))
 print(" group: raw->sigma", d(0, 1), " sigma->opfree", d(1, 2), " opfree->stores", d(2, 3), " stores->published", d(3, 4))
 print(" published->mma_start", d(4, 5), " mma_start->issued", d(5, 6), " tma_issue->raw_ready", d(7, 0))
 print(" group period (raw_ready[i+2]-raw_ready[i])", float(np.median((t[0][2:] - t[0][:-2])[20:n - 20])))
+
+ev = np.nonzero(flush_mask[:n])[0]
+ev = ev[(ev > 20) & (ev < n - 20)]
+print(" epilogue: flush wait->done median", float(np.median(t[9][ev] - t[8][ev])), " flush period", float(np.median(np.diff(t[8][ev]))))
+print(" mma_issued->next mma_start gaps (median over run starts vs others):",
+      float(np.median((t[5][1:] - t[6][:-1])[20:n-20])))

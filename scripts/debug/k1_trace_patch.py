@@ -6,7 +6,7 @@ Events per tile i of CTA 0 (group leaders: lane 0 of warps 0 and 4):
 p = "paper_2003_02978_b200/csrc/kernels.cuh"
 s = open(p).read()
 s = s.replace("""constexpr int kFlushTC = SMF_K1TC_FLUSH;""", """constexpr int kFlushTC = SMF_K1TC_FLUSH;
-__device__ unsigned long long g_k1trace[8][4096];
+__device__ unsigned long long g_k1trace[10][4096];
 #define K1TR(ev, i) do { if (blockIdx.x == 0 && (i) < 4096) g_k1trace[ev][(i)] = clock64(); } while (0)
 //""", 1)
 reps = [
@@ -33,6 +33,18 @@ reps = [
                 K1TR(6, i);"""),
     ("""                mbar_arrive_expect_tx(&raw_full[s], Raw::TX);""", """                mbar_arrive_expect_tx(&raw_full[s], Raw::TX);
                 K1TR(7, i);"""),
+    ("""            mbar_wait(&acc_full[ab], (g >> 1) & 1);
+            tc_fence_after();
+            const uint32_t t0 = tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)(ab * K::NCOL);""", """            mbar_wait(&acc_full[ab], (g >> 1) & 1);
+            if (lane == 0 && e == 0) K1TR(8, i);
+            tc_fence_after();
+            const uint32_t t0 = tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)(ab * K::NCOL);"""),
+    ("""            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            ++g;
+            if (col_end && live) {""", """            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            if (lane == 0 && e == 0) K1TR(9, i);
+            ++g;
+            if (col_end && live) {"""),
 ]
 for a, b in reps:
     assert a in s, a[:70]
