@@ -484,7 +484,10 @@ struct K1TC {
     static constexpr bool FITS = SMEM <= LIMIT && NCOL <= 256 && NEPI <= 3;
     static constexpr int TMEM_COLS = 2 * NCOL <= 32 ? 32 : 2 * NCOL <= 64 ? 64 : 2 * NCOL <= 128 ? 128
                                    : 2 * NCOL <= 256 ? 256 : 512;
-    static constexpr int NT = 13 * 32;
+    // warps 0-7 transform; 8-10 and 12-14 epilogue (TMEM lane quadrant wid % 4, column
+    // half wid / 12); 11 TMA; 15 MMA
+    static constexpr int NT = 16 * 32;
+    static constexpr int WTMA = 11, WMMA = 15;
     // transform split: part 0 quads [0, H0), part 1 quads [H0, NQ] (incl. the rho quad); H0 odd
     static constexpr int H0 = (NQ / 2) % 2 == 1 ? NQ / 2 : NQ / 2 + 1;
     static constexpr int HQ = (H0 > NQ + 1 - H0) ? H0 : NQ + 1 - H0;   // max quads per part
@@ -530,11 +533,11 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], K::NEPI);
+            mbar_init(&acc_empty[b], 2 * K::NEPI);
         }
         fence_mbar_init();
     }
-    if (wid == 12) tmem_alloc(&tmem_sh, K::TMEM_COLS);
+    if (wid == K::WMMA) tmem_alloc(&tmem_sh, K::TMEM_COLS);
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
@@ -658,9 +661,15 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&op_full[o]);
         }
-    } else if (wid >= 8 && wid < 8 + K::NEPI) {
+    } else if (wid >= 8 && wid != K::WTMA && wid != K::WMMA && (wid & 3) < K::NEPI) {
         // ===================== epilogue: TMEM -> fp64 shared accumulator -> partials =====================
-        const int e = wid - 8, m = 32 * e + lane;
+        // warp (quadrant e, half hf) folds rows 32 e .. 32 e + 31, 16-column chunks
+        // [n_lo, n_hi) of the two fp32 accumulators: D[:, :BE] + 2 D[:, BE:], pre-added in
+        // fp32 (one rounding, below the fp32 run's own) before the fp64 add. Two warps per
+        // quadrant: the trace showed the fold pacing the kernel with one.
+        const int e = wid & 3, hf = wid >= 12, m = 32 * e + lane;
+        constexpr int NCH = K::BE / 16, CH1 = (NCH + 1) / 2;
+        const int n_lo = hf ? 16 * CH1 : 0, n_hi = hf ? K::BE : 16 * CH1;
         const bool live = m < K::BE;
         double* arow = acc + (size_t)(live ? m : 0) * K::ACC_LD;
         TileCursor cur(tb, a.tpc);
@@ -677,12 +686,12 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
             tc_fence_after();
             const uint32_t t0 = tmem + ((uint32_t)(32 * e) << 16) + (uint32_t)(ab * K::NCOL);
 #pragma unroll 1
-            for (int n0 = 0; n0 < K::BE; n0 += 16) {
+            for (int n0 = n_lo; n0 < n_hi; n0 += 16) {
                 float v[16], u[16];
                 tmem_ld16x2(t0 + n0, t0 + K::BE + n0, v, u);
                 if (live && !(SMF_K1TC_EXP & 4)) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) arow[n0 + j] += (double)v[j] + 2.0 * (double)u[j];
+                    for (int j = 0; j < 16; ++j) arow[n0 + j] += (double)fmaf(2.f, u[j], v[j]);
                 }
             }
             tc_fence_before();
@@ -691,13 +700,13 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
             ++g;
             if (col_end && live) {
                 double* out = a.part1 + (((size_t)blockIdx.x * a.S + (c - cfirst)) * K::BE + m) * K::BE;
-                for (int n = 0; n < K::BE; ++n) {
+                for (int n = n_lo; n < n_hi; ++n) {
                     out[n] = arow[n];
                     arow[n] = 0.0;
                 }
             }
         }
-    } else if (wid == 11) {
+    } else if (wid == K::WTMA) {
         // ===================== TMA producer =====================
         if (lane == 0) {
             prefetch_tmap(&tm_main);
@@ -717,7 +726,7 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
                     tma_load_3d(st + Raw::NFULL * (kTileTC * 128), &tm_tail, &raw_full[s], Raw::NFULL * 32, row0, c);
             }
         }
-    } else if (wid == 12) {
+    } else if (wid == K::WMMA) {
         // ===================== MMA issuer (one thread) =====================
         if (lane == 0) {
             const uint32_t ops0 = smem_u32(ops);
@@ -752,7 +761,7 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (wid == 12) {
+    if (wid == K::WMMA) {
         tc_fence_after();
         tmem_dealloc(tmem, K::TMEM_COLS);
     }
