@@ -511,7 +511,6 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
     __shared__ uint64_t acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_sh;
     __shared__ __align__(16) float pil[8][B4];
-    __shared__ __align__(16) float gh[8][B4];
 
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     const long long tb = tile_begin(blockIdx.x, a.ttot, a.G), te = tile_begin(blockIdx.x + 1, a.ttot, a.G);
@@ -571,16 +570,22 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
         TileCursor cur(tb + grp, a.tpc);
         int ccol = -1;
         float4 pq[K::HQ];   // this thread's pilot quads, in registers (refreshed per column)
+        float kinv = 0.f;   // 1 / |c|^2: sigma = (L . c) / |c|^2 from the same registers
         for (int i = grp; i < ntl; i += 2) {
             const int c = cur.c, row0 = cur.tt * kTileTC;
             cur.next();
             cur.next();
             if (c != ccol) {
                 __syncwarp();
+                float cc = 0.f;
                 for (int b = lane; b < B4; b += 32) {
-                    pil[wid][b] = a.pil32[(size_t)c * a.B + b];
-                    gh[wid][b] = a.ghat32[(size_t)c * a.B + b];
+                    const float pv = a.pil32[(size_t)c * a.B + b];
+                    pil[wid][b] = pv;
+                    cc = fmaf(pv, pv, cc);
                 }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) cc += __shfl_xor_sync(0xffffffffu, cc, off);
+                kinv = cc > 0.f ? 1.f / cc : 0.f;
                 __syncwarp();
 #pragma unroll
                 for (int q = 0; q < K::HQ; ++q)
@@ -604,11 +609,12 @@ __global__ void __launch_bounds__(K1TC<NQ>::NT, 1)
             for (int q = 0; q < K::HQ; ++q) {
                 if (q < nqp && q0 + q < NQ) {
                     v[q] = lds4(raw0 + s * Raw::STAGE + qo[q]);
-                    sgp[q & 3] = dot4(v[q], *reinterpret_cast<const float4*>(&gh[wid][4 * (q0 + q)]), sgp[q & 3]);
+                    sgp[q & 3] = dot4(v[q], pq[q], sgp[q & 3]);
                 }
             }
             float sg = (sgp[0] + sgp[1]) + (sgp[2] + sgp[3]);
             sg += __shfl_xor_sync(0xffffffffu, sg, 16);
+            sg *= kinv;   // sigma = L . c / |c|^2 (any sigma reconstructs exactly, DESIGN 6.1)
             int ok = 1;   // nodata masking: both halves of the row must be valid
             if (a.mask) {
 #pragma unroll
