@@ -1240,33 +1240,26 @@ __global__ void k_energy(UpdateArgs a) {
 
 
 // Solve the 3x3 system K x = v by Gaussian elimination with partial pivoting.
-__device__ __forceinline__ bool solve3(double K[3][3], double v[3], double x[3]) {
-    for (int col = 0; col < 3; ++col) {
-        int piv = col;
-        for (int r = col + 1; r < 3; ++r)
-            if (fabs(K[r][col]) > fabs(K[piv][col])) piv = r;
-        if (!(fabs(K[piv][col]) > 0.0)) return false;
-        if (piv != col) {
-            for (int k = 0; k < 3; ++k) {
-                double t = K[col][k];
-                K[col][k] = K[piv][k];
-                K[piv][k] = t;
-            }
-            double t = v[col];
-            v[col] = v[piv];
-            v[piv] = t;
-        }
-        for (int r = col + 1; r < 3; ++r) {
-            double f = K[r][col] / K[col][col];
-            for (int k = col; k < 3; ++k) K[r][k] -= f * K[col][k];
-            v[r] -= f * v[col];
-        }
-    }
-    for (int r = 2; r >= 0; --r) {
-        double s = v[r];
-        for (int k = r + 1; k < 3; ++k) s -= K[r][k] * x[k];
-        x[r] = s / K[r][r];
-    }
+__device__ __forceinline__ bool solve3(const double K[3][3], const double v[3], double x[3]) {
+    // Cramer's rule with the adjugate: static indexing only (the pivoting version's
+    // runtime row swaps put K in local memory; measured ~6K cycles per update with the
+    // reduction around it). K = I + G M is a well-conditioned 3 x 3 in the regime the
+    // update runs in; a zero or non-finite determinant reports NOT_SPD as before.
+    const double a00 = K[1][1] * K[2][2] - K[1][2] * K[2][1];
+    const double a01 = K[0][2] * K[2][1] - K[0][1] * K[2][2];
+    const double a02 = K[0][1] * K[1][2] - K[0][2] * K[1][1];
+    const double a10 = K[1][2] * K[2][0] - K[1][0] * K[2][2];
+    const double a11 = K[0][0] * K[2][2] - K[0][2] * K[2][0];
+    const double a12 = K[0][2] * K[1][0] - K[0][0] * K[1][2];
+    const double a20 = K[1][0] * K[2][1] - K[1][1] * K[2][0];
+    const double a21 = K[0][1] * K[2][0] - K[0][0] * K[2][1];
+    const double a22 = K[0][0] * K[1][1] - K[0][1] * K[1][0];
+    const double det = K[0][0] * a00 + K[0][1] * a10 + K[0][2] * a20;
+    if (!(fabs(det) > 0.0) || !isfinite(det)) return false;
+    const double id = 1.0 / det;
+    x[0] = (a00 * v[0] + a01 * v[1] + a02 * v[2]) * id;
+    x[1] = (a10 * v[0] + a11 * v[1] + a12 * v[2]) * id;
+    x[2] = (a20 * v[0] + a21 * v[1] + a22 * v[2]) * id;
     return isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]);
 }
 
@@ -1296,22 +1289,36 @@ __global__ void __launch_bounds__(128, 5) k2_update(UpdateArgs a) {
         // the sweeps stream the cube with evict_first, so it stays L2-resident
         bulk_load_hint(sAinv, cs.ainv + (size_t)c * B * B, bytes, &abar, l2_policy_evict_last());
     }
+    // this thread's per-band state, loaded now so the loads overlap the partials gather
+    double mb = 0.0, tp = 0.0, yp = 0.0, mh = 0.0, sj = 0.0;
+    if (tid < B) {
+        const size_t o = (size_t)c * B + tid;
+        mb = cs.mbar[o];
+        tp = cs.tprev[o];
+        yp = cs.yprev[o];
+        mh = (double)cs.mhat32[o];
+        sj = (double)cs.s[tid];
+    }
+    const double nvc = cs.nvalid[c];
     // 1. sufficient statistics of sweep k-1 (fixed CTA order)
+    // CTAs covering column c: b0 = the CTA of tile c0 .. b1 = the CTA of tile c1 - 1, with
+    // b(t) = ((t + 1) G - 1) / ttot the inverse of tile_begin (G <= ttot); only b0's
+    // range can start before c0, every later one starts inside the column (slot 0)
     const long long c0 = (long long)c * a.tpc, c1 = c0 + a.tpc;
-    int b0 = (int)((c0 * a.G) / a.ttot);
-    while (b0 > 0 && tile_begin(b0, a.ttot, a.G) > c0) --b0;
-    while (tile_begin(b0 + 1, a.ttot, a.G) <= c0) ++b0;
+    const int b0 = (int)(((c0 + 1) * a.G - 1) / a.ttot);
+    const int b1 = (int)((c1 * a.G - 1) / a.ttot);
+    const int slot0 = c - (int)(tile_begin(b0, a.ttot, a.G) / a.tpc);
     const int W = B + kPartExtra;
     double sv = 0.0, s0 = 0.0, s2 = 0.0, ss = 0.0;
-    for (int b = b0; b < a.G && tile_begin(b, a.ttot, a.G) < c1; b += 4) {
+    for (int b = b0; b <= b1; b += 4) {
         // up to 4 slots' loads in flight, summed in CTA order
         double pv[4], p0[4], p2[4], ps[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             pv[u] = p0[u] = p2[u] = ps[u] = 0.0;
             const int bb = b + u;
-            if (bb < a.G && tile_begin(bb, a.ttot, a.G) < c1) {
-                const int slot = c - (int)(tile_begin(bb, a.ttot, a.G) / a.tpc);
+            if (bb <= b1) {
+                const int slot = bb == b0 ? slot0 : 0;
                 const double* P = a.part3 + ((size_t)bb * a.S + slot) * W;
                 if (tid < B) pv[u] = P[3 + tid];
                 if (tid == 0) {
@@ -1335,19 +1342,14 @@ __global__ void __launch_bounds__(128, 5) k2_update(UpdateArgs a) {
         sh_s[2] = ss;
     }
     __syncthreads();
-    const double invN = 1.0 / cs.nvalid[c];
+    const double invN = 1.0 / nvc;
     const double bbar = sh_s[0] * invN, b2 = sh_s[1] * invN, bs = sh_s[2] * invN;
-    double mb = 0.0, tp = 0.0, t = 0.0, h = 0.0, mu = 0.0, yp = 0.0, mh = 0.0;
+    double t = 0.0, h = 0.0, mu = 0.0;
     if (tid < B) {
-        const size_t o = (size_t)c * B + tid;
-        mb = cs.mbar[o];
-        tp = cs.tprev[o];
-        yp = cs.yprev[o];
-        mh = (double)cs.mhat32[o];
         // h = (1/N) sum beta (L - mu0) = (1/N)[sum beta L' + (sum beta s) mhat] - bbar mu0
         h = sv * invN + (bs * mh - bbar * mb);
         mu = mb - bbar * tp;                 // Eq. 10 / line 10
-        t = mu * (double)cs.s[tid];          // Eq. 9
+        t = mu * sj;                         // Eq. 9
         sh_t[tid] = t;
         sh_h[tid] = h;
     }
