@@ -946,16 +946,29 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
         }
         __syncthreads();
         const int ns = sh_nslot;
-        for (int i = tid; i < a.W1; i += blockDim.x) {
-            double t = 0.0;
-            for (int q0 = 0; q0 < ns; q0 += 8) {   // 8 independent loads, summed in slot order
-                double v[8];
+        // 4 entries x 2 slots = 8 independent loads per round (a column spans 1-2 K1 CTAs
+        // at the flightline shape, so rounds over entries, not slots, carry the latency;
+        // the phase trace had this gather at 16 % of k2_init), each entry summed in slot order
+        const int bd = blockDim.x;
+        for (int i = tid; i < a.W1; i += 4 * bd) {
+            double t[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int q0 = 0; q0 < ns; q0 += 2) {
+                double v[2][4];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) v[q] = q0 + q < ns ? a.part1[sh_slot[q0 + q] + i] : 0.0;
+                for (int q = 0; q < 2; ++q)
 #pragma unroll
-                for (int q = 0; q < 8; ++q) t += v[q];
+                    for (int u = 0; u < 4; ++u) {
+                        const int idx = i + u * bd;
+                        v[q][u] = (q0 + q < ns && idx < a.W1) ? a.part1[sh_slot[q0 + q] + idx] : 0.0;
+                    }
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) t[u] += v[q][u];
             }
-            S[i] = t;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + u * bd < a.W1) S[i + u * bd] = t[u];
         }
     }
     if (tid == 0) bad = COL_OK;
