@@ -440,3 +440,35 @@ def test_graph_mode_is_bitwise_eager(smf, torch):
     side.synchronize()
     np.testing.assert_array_equal(enh.cpu().numpy(), e5)
     np.testing.assert_array_equal(alb.cpu().numpy(), a5)
+
+
+_SWITCH_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2003_02978_b200 import smf, synth
+cfg = synth.scaled(synth.CONFIGS["segment"], cols=6, pixels=1500)
+cube, s, _ = synth.generate(cfg)
+r = smf.Retriever(cfg.bands, s, n_iter=10)
+enh, alb, st = r.retrieve(torch.from_numpy(cube).cuda())
+torch.cuda.synchronize()
+np.save(sys.argv[2], np.stack([enh.cpu().numpy(), alb.cpu().numpy()]))
+"""
+
+
+@pytest.mark.parametrize("env", [{"SMF_PDL": "0"}, {"SMF_SERPENTINE": "0"}, {"SMF_L2KEEP_MB": "0"}],
+                         ids=["no_pdl", "forward_sweeps", "no_l2_hints"])
+def test_ab_switches_keep_parity(smf, torch, tmp_path, env):
+    """The runtime A/B switches (DESIGN 8a) select other launch/scheduling paths; each must
+    keep parity with the oracle (they are read once per process, so a subprocess runs)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "o.npy"
+    subprocess.run([sys.executable, "-c", _SWITCH_SCRIPT, root, str(out)], check=True, timeout=300,
+                   env={**os.environ, **env})
+    enh, alb = np.load(out)
+    cfg = synth.scaled(synth.CONFIGS["segment"], cols=6, pixels=1500)
+    cube, s, _ = synth.generate(cfg)
+    a_ref, r_ref, st_ref = oracle.retrieve(cube, s, n_iter=10)
+    print(assert_parity(enh, alb, a_ref, r_ref, f"switch {env}"))
