@@ -659,7 +659,10 @@ __host__ inline size_t k3w_smem(int B) {
 template <int J, bool MASK>
 __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const float* L) {
     constexpr int NW = kWideNT3 / 32;
-    constexpr int PB = J >= 20 ? 1 : 2;   // pixels per warp pass (registers: PB x J row elements)
+#ifndef SMF_K3W_PB
+#define SMF_K3W_PB 4
+#endif
+    constexpr int PB = J >= 20 ? 1 : (J <= 14 ? SMF_K3W_PB : 2);   // pixels per warp pass (registers: PB x J row elements)
     extern __shared__ __align__(16) float w4_smem[];
     const int B = a.B, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const size_t TF = k3w_tile_floats(B);
