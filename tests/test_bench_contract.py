@@ -20,3 +20,25 @@ def test_reference_arm_json_contract():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_contract():
+    """The GPU arm's line: roofline (bound, achieved, peak, unit, frac, traffic), clocks,
+    gpu_launches, and an end-to-end number with the H2D/D2H bytes it moved."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "2", "--warmup", "3",
+                          "--e2e-steps", "1", "--no-cpu-baseline"], capture_output=True, text=True, timeout=900,
+                         cwd=ROOT, check=True)
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3 and d["value"] > 0
+    r = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert d["gpu_launches"] == 2 * 65   # K0, K1, K2-init, 31 sweeps, 30 updates, status copy
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 598 * 20000 * 72 * 4 and e["d2h_bytes_per_step"] > 0
