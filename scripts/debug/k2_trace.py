@@ -15,8 +15,8 @@ buf = np.zeros(64 * 8, dtype=np.uint64)
 smf._lib.smf_debug_k2_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 assert smf._lib.smf_debug_k2_trace(buf.ctypes.data, buf.size) == 0
 t = buf.reshape(64, 8).astype(np.int64)
-d = np.diff(t[:, :7], axis=1)
-names = ["gather+sync", "t/h setup", "matvec (incl. A^-1 wait)", "G setup", "block_sum G + solve", "z + qc sum"]
+d = np.diff(t[:, :6], axis=1)
+names = ["gather + sync", "t/h setup + sync", "mat-vec (A^-1 wait incl.)", "G sums + solve + sync", "z + q sums"]
 for k, nme in enumerate(names):
     print(f"{nme:28s} median {np.median(d[:, k]):8.0f} cycles")
-print("total (start->end) median", np.median(t[:, 6] - t[:, 0]))
+print("total (start->end) median", np.median(t[:, 5] - t[:, 0]))
