@@ -113,7 +113,8 @@ int smf_supported_bands(int bands);
 /* The retrieval. Validates host-side arguments synchronously, enqueues every
  * step on `stream` (all arithmetic in this library's CUDA kernels) and
  * returns without synchronising.
- *   radiance      device fp32 [cols][pixels][bands], read-only, 16-byte aligned
+ *   radiance      device fp32 [cols][pixels][bands], read-only, 16-byte aligned when
+ *                 bands % 4 == 0 and bands <= 96 (TMA path), else 4-byte aligned
  *   enhancement   device fp32 [cols][pixels] out: alpha^{N_iter} in ppm m
  *   albedo        device fp32 [cols][pixels] out: raw r_i (Eq. 7), 1 if albedo off
  *   workspace     device, >= smf_workspace_bytes(cols, pixels), 256-byte aligned
@@ -157,10 +158,11 @@ smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols,
  * NULL pointer or cols < 1. */
 smf_status smf_host_chunk_cols(const smf_ctx* ctx, int cols, int* chunk_cols);
 
-/* Per-column background model after the last smf_retrieve that used
- * `workspace`: mu^{N_iter} (device fp64 [cols][bands], or NULL) and
- * q^{N_iter} = t^T (C+rho I)^-1 t (device fp64 [cols], or NULL). Enqueued on
- * `stream`. */
+/* Per-partition background model after the last smf_retrieve (N_iter >= 1) that used
+ * `workspace`: mu^{N_iter} (device fp64 [partitions][bands], or NULL) and
+ * q^{N_iter} = t^T (C+rho I)^-1 t (device fp64 [partitions], or NULL); partitions =
+ * cols without grouping, else the full groups then the remainder (smf_group_partitions).
+ * Enqueued on `stream`. */
 smf_status smf_column_model(smf_ctx* ctx, const void* workspace, int cols, int pixels,
                             double* mu_out, double* q_out, void* stream);
 
@@ -211,8 +213,8 @@ smf_status smf_convert_layout(const float* in, int lines, int samples, int bands
  * Layouts are unchanged ([cols][pixels][bands] in, [cols][pixels] out, column_status
  * per column = the status of its partition); smf_workspace_bytes accounts for the
  * grouping; smf_energy_trace then returns [N_iter + 1][partitions]. G = 1 (default)
- * is one partition per column. smf_column_model and smf_initial_statistics
- * always treat each column as a partition.
+ * is one partition per column. smf_column_model reports per partition;
+ * smf_initial_statistics always treats each column as a partition.
  * smf_group_partitions: number of partitions and (optional, host int[n]) the first
  * column of each. */
 smf_status smf_set_grouping(smf_ctx* ctx, int group);
@@ -234,6 +236,37 @@ smf_status smf_group_partitions(int cols, int group, int* n_partitions, int* fir
 smf_status smf_set_energy_trace(smf_ctx* ctx, int enable);
 smf_status smf_energy_trace(smf_ctx* ctx, const void* workspace, int cols, int pixels, double* energy_out,
                             void* stream);
+
+/* Per-iteration positive-definiteness of C^k + rho I (Fig. alg lines 14-16; the
+ * oracle factors every C^k and reports a Cholesky pivot <= bands * 2^-52 * max diag as
+ * SMF_COL_NOT_SPD, reading C16'). The hot path never forms C^k: it applies the
+ * exact rank-3 identity C^k = C0 + U M U^T through a Woodbury solve on (C0 + rho I)^-1, whose
+ * fp32-statistics precision cannot resolve a collapse of C^k below ~1e-6 of C0. So each
+ * iteration also computes the smallest eigenvalue of (C0+rho I)^-1 (C^k+rho I) from the 3 x 3
+ * Woodbury capacitance, and when it is <= 1e-3 (mode SMF_COVCHECK_AUTO, default) or always
+ * (SMF_COVCHECK_ALWAYS) the column's iteration is done literally in fp64, as the oracle does
+ * it (reading C16''): mu^k from line 10, C^k = (1/N) sum d_i d_i^T from the residuals (lines
+ * 12-14), a Cholesky with the oracle's pivot criterion (NOT_SPD on failure), and z^k, q^k from
+ * its triangular solves. SMF_COVCHECK_OFF keeps only the Woodbury path (NOT_SPD when its 3 x 3
+ * capacitance is exactly singular) -- for measurement. Realistic columns never trigger the
+ * literal path (smallest eigenvalue >= 0.03 on every config measured), so it costs nothing
+ * there; a triggered column costs O(N bands^2) fp64 work in its update kernel. */
+enum { SMF_COVCHECK_OFF = 0, SMF_COVCHECK_AUTO = 1, SMF_COVCHECK_ALWAYS = 2 };
+smf_status smf_set_covariance_check(smf_ctx* ctx, int mode);
+
+/* Per-iteration diagnostics (the exact-zero fraction of P:733-736).
+ * When enabled (enable != 0; default off), smf_retrieve records after every sweep
+ * k = 0..N_iter, per partition: the number of pixels with alpha_i^k > 0, q^k = t^T (C^k+rho
+ * I)^-1 t, the partition status, and the cumulative number of iterations whose C^k was
+ * recomputed literally (smf_set_covariance_check). One extra small kernel per sweep (it reads
+ * the [cols][pixels] enhancement map once). smf_iteration_diagnostics copies the records of
+ * the last smf_retrieve that used `workspace` to caller device buffers laid out
+ * [N_iter + 1][partitions] (any pointer may be NULL), enqueued on `stream`;
+ * SMF_ERR_NOT_CONFIGURED if diagnostics were not enabled. The workspace size depends on this
+ * switch and N_iter (query smf_workspace_bytes after setting them). */
+smf_status smf_set_diagnostics(smf_ctx* ctx, int enable);
+smf_status smf_iteration_diagnostics(smf_ctx* ctx, const void* workspace, int cols, int pixels, int64_t* nnz_out,
+                                     double* q_out, int32_t* status_out, int32_t* literal_out, void* stream);
 
 /* Kernel launches enqueued by the last smf_retrieve call on this context. */
 int smf_last_launch_count(const smf_ctx* ctx);

@@ -848,6 +848,7 @@ struct ColState {
     double* rho64;    // [cols]
     double* tq;       // [cols]
     double* nvalid;   // [cols] pixels in the partition's statistics (N, or the valid count when masking)
+    int* nlit;        // [cols] iterations whose C^k was recomputed literally (reading C16'', diagnostic)
     int mask;         // nodata masking on
     float nodata;     // nodata value (masking)
 };
@@ -1156,6 +1157,7 @@ __global__ void __launch_bounds__(256) k2_init(InitArgs a) {
         a.cs.kc32[2 * c] = (float)qc[1];
         a.cs.kc32[2 * c + 1] = (float)qc[2];
         a.cs.status[c] = st;
+        a.cs.nlit[c] = 0;
         double tra = 0.0;   // tr((C0 + rho I)^-1) for the energy trace
         for (int b = 0; b < B; ++b) tra += A[b * B + b];
         a.cs.tra[c] = tra;
@@ -1178,7 +1180,202 @@ struct UpdateArgs {
     int cols, N, B, tpc, G, S, k;
     int energy_on;         // compute T_k (energy trace) in the update
     long long ttot;
+    // literal covariance check (reading C16''): C^k recomputed from the residuals, Cholesky-
+    // factored with the oracle's pivot criterion, when the Woodbury capacitance says C^k + rho I
+    // is within kLitTau of singular relative to A0 (lit_mode 1), always (2) or never (0)
+    const float* L;        // radiance of this plan [cols][N][B]
+    const float* enh;      // alpha^{k-1} [cols][N] (the previous sweep's output)
+    const float* alb;      // raw albedo r [cols][N]
+    double* lit;           // wide path: per-column fp64 scratch of lit_stride doubles (narrow: smem)
+    long long lit_stride;
+    float r_floor;
+    int use_albedo;
+    int lit_mode;
 };
+
+// Trigger of the literal check: the smallest eigenvalue of A0^-1 (C^k + rho I) below 1 equals the
+// smallest eigenvalue of the 3 x 3 capacitance K = I + G M (C^k + rho I = A0 + U M U^T, G = U^T
+// A0^-1 U). Every realistic column measured stays >= 0.03 over 30 iterations (segment, tiny,
+// campaign 5 %), so the literal path costs nothing on the benchmark workloads.
+constexpr double kLitTau = 1e-3;
+
+// Smallest eigenvalue of a 3 x 3 matrix with a real spectrum (K = I + G M with G psd and M
+// symmetric is similar to the symmetric I + G^1/2 M G^1/2): trigonometric root of the
+// characteristic cubic. NaN in -> NaN out.
+__device__ inline double min_eig3(const double K[3][3]) {
+    const double tr = K[0][0] + K[1][1] + K[2][2];
+    const double c2 = (K[0][0] * K[1][1] - K[0][1] * K[1][0]) + (K[0][0] * K[2][2] - K[0][2] * K[2][0]) +
+                      (K[1][1] * K[2][2] - K[1][2] * K[2][1]);
+    const double det = K[0][0] * (K[1][1] * K[2][2] - K[1][2] * K[2][1]) -
+                       K[0][1] * (K[1][0] * K[2][2] - K[1][2] * K[2][0]) +
+                       K[0][2] * (K[1][0] * K[2][1] - K[1][1] * K[2][0]);
+    // lambda^3 + a lambda^2 + b lambda + c = 0 with a = -tr, b = c2, c = -det
+    const double a3 = -tr / 3.0;
+    const double Q = a3 * a3 - c2 / 3.0;
+    const double R = a3 * a3 * a3 - a3 * c2 / 2.0 - det / 2.0;
+    if (!(Q > 0.0)) return isfinite(Q) ? -a3 : Q;   // triple root (or NaN)
+    const double sq = sqrt(Q);
+    const double x = fmin(1.0, fmax(-1.0, R / (Q * sq)));
+    return -2.0 * sq * cos(acos(x) / 3.0) - a3;
+}
+
+// lower-triangle packed index (i >= j)
+__device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }
+__device__ __forceinline__ void pk_decode(int e, int& i, int& j) {
+    i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+    while (pk(i + 1, 0) <= e) ++i;
+    while (pk(i, 0) > e) --i;
+    j = e - pk(i, 0);
+}
+
+// One iteration's lines 10-16 done literally, as the oracle does them (reading C16''):
+//   mu^k = (1/N) sum (L_i - r~_i alpha_i^{k-1} t^{k-1}),  t^k = mu^k (.) s          (line 10, Eq. 9)
+//   d_i = L_i - r~_i alpha_i^{k-1} t^k - mu^k,  C^k = (1/N) sum d_i d_i^T             (lines 12-14)
+//   Cholesky of C^k + rho I; a pivot <= B 2^-52 max diag (or non-finite) -> NOT_SPD (C16')
+//   z^k = (C^k + rho I)^-1 t^k, q^k = t^k . z^k, c^k = mu^k . z^k                      (line 16)
+// all in fp64 from the fp32 radiances and the fp32 alpha^{k-1}, r of the previous sweep.
+// Writes the column's z32, t^k (tprev), A0^-1 t^k (yprev), mu^k, q, (mhat.z, mu.z), status.
+// Cp: packed lower C (B(B+1)/2 doubles), D: P x B doubles of residual rows (reused as the
+// solve's right-hand side), both shared or global; A0inv: (C0 + rho I)^-1 (read before Cp/D are
+// written, so the narrow path may alias them onto its A0^-1 staging); sv: smem [2][B];
+// scratch: smem >= [32][3] doubles. Called by the whole block; returns the column status.
+__device__ int literal_iteration(const UpdateArgs& a, int c, const double* A0inv, double* Cp, double* D, int P,
+                                 double* sv, double* scratch) {
+    const ColState& cs = a.cs;
+    const int B = a.B, tid = threadIdx.x, nt = blockDim.x, N = a.N;
+    const size_t pix0 = (size_t)c * N;
+    const float* Lc = a.L + pix0 * B;
+    const float* al = a.enh + pix0;
+    const float* rr = a.alb + pix0;
+    const double nvc = cs.nvalid[c];
+    double* mu = sv;        // [B]
+    double* t = sv + B;     // [B]
+    auto beta_of = [&](int i, bool& ok) -> double {
+        const float ai = al[i];
+        ok = ai == ai;   // nodata pixels carry NaN alpha and take no part (reading C22)
+        const float rt = a.use_albedo ? fmaxf(rr[i], a.r_floor) : 1.f;
+        return (double)rt * (double)ai;
+    };
+    // line 10 (t' = t^{k-1} as the previous update left it)
+    for (int b = tid; b < B; b += nt) {
+        const double tpb = cs.tprev[(size_t)c * B + b];
+        double acc = 0.0;
+        for (int i = 0; i < N; ++i) {
+            bool ok;
+            const double be = beta_of(i, ok);
+            if (ok) acc += (double)Lc[(size_t)i * B + b] - be * tpb;
+        }
+        mu[b] = acc / nvc;
+        t[b] = mu[b] * (double)cs.s[b];
+    }
+    __syncthreads();
+    // A0^-1 t^k for the next iteration's Woodbury (y' of U = [t', t, h])
+    for (int b = tid; b < B; b += nt) {
+        double y = 0.0;
+        for (int i = 0; i < B; ++i) y = fma(A0inv[(size_t)i * B + b], t[i], y);
+        cs.yprev[(size_t)c * B + b] = y;
+    }
+    __syncthreads();
+    // lines 12-14: C^k = (1/N) sum d_i d_i^T, P residual rows at a time
+    const int E = B * (B + 1) / 2;
+    for (int e = tid; e < E; e += nt) Cp[e] = 0.0;
+    for (int p0 = 0; p0 < N; p0 += P) {
+        const int np = min(P, N - p0);
+        __syncthreads();
+        for (int x = tid; x < np * B; x += nt) {
+            const int p = x / B, b = x - p * B, i = p0 + p;
+            bool ok;
+            const double be = beta_of(i, ok);
+            D[x] = ok ? ((double)Lc[(size_t)i * B + b] - be * t[b]) - mu[b] : 0.0;
+        }
+        __syncthreads();
+        for (int e = tid; e < E; e += nt) {
+            int i, j;
+            pk_decode(e, i, j);
+            double s = 0.0;
+            for (int p = 0; p < np; ++p) s = fma(D[p * B + i], D[p * B + j], s);
+            Cp[e] += s;
+        }
+    }
+    __syncthreads();
+    // ridge and the pivot tolerance (oracle_cholesky: n 2^-52 max_i A_ii)
+    double dmax = 0.0;
+    for (int b = tid; b < B; b += nt) {
+        const int e = pk(b, b);
+        dmax = fmax(dmax, Cp[e] / nvc + cs.rho64[c]);
+    }
+    for (int off = 16; off > 0; off >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
+    if ((tid & 31) == 0) scratch[tid >> 5] = dmax;
+    for (int e = tid; e < E; e += nt) {
+        int i, j;
+        pk_decode(e, i, j);
+        Cp[e] = Cp[e] / nvc + (i == j ? cs.rho64[c] : 0.0);
+    }
+    __syncthreads();
+    dmax = 0.0;
+    for (int w = 0; w < (nt + 31) / 32; ++w) dmax = fmax(dmax, scratch[w]);
+    const double tol = (double)B * 2.220446049250313e-16 * dmax;
+    __syncthreads();
+    // right-looking Cholesky in place (same subtraction order per entry as the oracle's
+    // left-looking loops: k = 0 .. j-1)
+    for (int j = 0; j < B; ++j) {
+        const double d = Cp[pk(j, j)];
+        if (!(d > tol) || !isfinite(d)) return COL_NOT_SPD;   // uniform: every thread read d
+        const double g = sqrt(d);
+        __syncthreads();
+        for (int i = j + 1 + tid; i < B; i += nt) Cp[pk(i, j)] /= g;
+        if (tid == 0) Cp[pk(j, j)] = g;
+        __syncthreads();
+        const int m = B - j - 1, cnt = m * (m + 1) / 2;
+        for (int e = tid; e < cnt; e += nt) {
+            int ii, ll;
+            pk_decode(e, ii, ll);
+            const int i = j + 1 + ii, l = j + 1 + ll;
+            Cp[pk(i, l)] -= Cp[pk(i, j)] * Cp[pk(l, j)];
+        }
+        __syncthreads();
+    }
+    // z = (G G^T)^-1 t: forward then back substitution, column-oriented
+    double* x = D;
+    for (int b = tid; b < B; b += nt) x[b] = t[b];
+    __syncthreads();
+    for (int j = 0; j < B; ++j) {
+        const double yj = x[j] / Cp[pk(j, j)];
+        __syncthreads();
+        for (int i = j + 1 + tid; i < B; i += nt) x[i] -= Cp[pk(i, j)] * yj;
+        if (tid == 0) x[j] = yj;
+        __syncthreads();
+    }
+    for (int j = B - 1; j >= 0; --j) {
+        const double xj = x[j] / Cp[pk(j, j)];
+        __syncthreads();
+        for (int i = tid; i < j; i += nt) x[i] -= Cp[pk(j, i)] * xj;
+        if (tid == 0) x[j] = xj;
+        __syncthreads();
+    }
+    double qc[3] = {0.0, 0.0, 0.0};
+    for (int b = tid; b < B; b += nt) {
+        const size_t o = (size_t)c * B + b;
+        const float z32 = (float)x[b];
+        qc[0] += t[b] * x[b];
+        qc[1] += (double)cs.mhat32[o] * (double)z32;
+        qc[2] += mu[b] * (double)z32;
+        cs.z32[o] = z32;
+        cs.tprev[o] = t[b];
+        cs.mu[o] = mu[b];
+    }
+    block_sum<3>(qc, scratch);
+    const int st = (!(qc[0] > 0.0) || !isfinite(qc[0]) || !isfinite(qc[1]) || !isfinite(qc[2]))
+                       ? COL_DEGENERATE_TARGET
+                       : COL_OK;
+    if (tid == 0) {
+        cs.q64[c] = qc[0];
+        cs.q32[c] = (float)qc[0];
+        cs.kc32[2 * c] = (float)qc[1];
+        cs.kc32[2 * c + 1] = (float)qc[2];
+    }
+    return st;
+}
 
 // Woodbury pieces shared by the narrow and wide updates: with U = [t', t, h],
 // Y = A0^-1 U, G = U^T Y, YY = Y^T Y and M the rank-3 coefficient matrix,
@@ -1252,7 +1449,7 @@ __global__ void k_energy(UpdateArgs a) {
 }
 
 
-// Solve the 3x3 system K x = v by Gaussian elimination with partial pivoting.
+// Solve the 3x3 system K x = v (Cramer's rule with the adjugate).
 __device__ __forceinline__ bool solve3(const double K[3][3], const double v[3], double x[3]) {
     // Cramer's rule with the adjugate: static indexing only (the pivoting version's
     // runtime row swaps put K in local memory; measured ~6K cycles per update with the
@@ -1282,11 +1479,13 @@ __global__ void __launch_bounds__(128, 5) k2_update(UpdateArgs a) {
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x;
     extern __shared__ double sAinv[];   // [B][B] A^-1 of this column (bulk copy)
     __shared__ uint64_t abar;
-    __shared__ double sh_t[128], sh_h[128];
+    __shared__ double sh_th[256];   // t^k, h (the literal check reuses it for mu^k, t^k)
+    double* sh_t = sh_th;
+    double* sh_h = sh_th + 128;
     __shared__ double scratch[(128 / 32) * 18];
     __shared__ double sh_coef[3];
     __shared__ double sh_s[3];
-    __shared__ int sh_st;
+    __shared__ int sh_st, sh_lit;
     griddep_wait();
     ColState& cs = a.cs;
     const int st0 = cs.status[c];
@@ -1408,16 +1607,29 @@ __global__ void __launch_bounds__(128, 5) k2_update(UpdateArgs a) {
             v[i] = gv[i * 3 + 1];   // u_i^T A^-1 t
         }
         int st = COL_OK;
-        if (!solve3(K, v, x)) st = COL_NOT_SPD;
+        const bool solved = solve3(K, v, x);
+        if (!solved) st = COL_NOT_SPD;
         for (int i = 0; i < 3; ++i) {
             double s = 0.0;
             for (int l = 0; l < 3; ++l) s += M[i][l] * x[l];
             sh_coef[i] = s;
         }
         sh_st = st;
+        sh_lit = a.lit_mode == 2 || (a.lit_mode == 1 && (!solved || !(min_eig3(K) > kLitTau)));
         if (a.energy_on) cs.tq[c] = woodbury_trace(M, gv, gv + 9, B, cs.rho64[c], cs.tra[c], bbar);
     }
     __syncthreads();
+    if (sh_lit) {
+        // C^k + rho I within kLitTau of singular relative to A0: lines 10-16 literally (reading
+        // C16''); A^-1's smem copy becomes the packed C^k and its residual-row buffer
+        const int E = B * (B + 1) / 2;
+        const int stl = literal_iteration(a, c, sAinv, sAinv, sAinv + E, (B * B - E) / B, sh_th, scratch);
+        if (tid == 0) {
+            cs.status[c] = stl;
+            cs.nlit[c] += 1;
+        }
+        return;
+    }
     // 4. z = y_t - Y M (I + G M)^-1 U^T A^-1 t   (Woodbury)
     double z = 0.0;
     float z32 = 0.f;
@@ -1454,7 +1666,6 @@ struct SweepArgs {
     const float* mhat32;
     const float* kc32;
     const float* q32;
-    const double* mm64;    // unused placeholder (|mu0|^2 derived from mhat)
     const int* status;
     double* part3;         // [G][S][B+3]
     int cols, N, B, tpc, G, S;
@@ -1707,24 +1918,41 @@ __global__ void k_copy_status(const int* src, int32_t* dst, int n) {
     if (i < n) dst[i] = src[i];
 }
 
+// Per-iteration diagnostics (the exact-zero fraction of P:733-736): after sweep k,
+// the column's count of alpha_i^k > 0, q^k, status and cumulative literal-check count.
+struct DiagArgs {
+    const float* enh;
+    ColState cs;
+    long long* nnz;   // [n_iter+1][cols]
+    double* q;
+    int* st;
+    int* lit;
+    int cols, N, k;
+};
+__global__ void __launch_bounds__(256) k_diag(DiagArgs a) {
+    const int c = blockIdx.x, tid = threadIdx.x;
+    const float* al = a.enh + (size_t)c * a.N;
+    unsigned n = 0;
+    for (int i = tid; i < a.N; i += blockDim.x) n += al[i] > 0.f ? 1u : 0u;
+    for (int off = 16; off > 0; off >>= 1) n += __shfl_xor_sync(0xffffffffu, n, off);
+    __shared__ unsigned red[8];
+    if ((tid & 31) == 0) red[tid >> 5] = n;
+    __syncthreads();
+    if (tid == 0) {
+        long long tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+        const size_t o = (size_t)a.k * a.cols + c;
+        a.nnz[o] = tot;
+        a.q[o] = a.cs.q64[c];
+        a.st[o] = a.cs.status[c];
+        a.lit[o] = a.cs.nlit[c];
+    }
+}
+
 // detector grouping: column c takes the status of its partition c / G
 __global__ void k_expand_status(const int32_t* part_status, int32_t* dst, int cols, int G) {
     int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c < cols) dst[c] = part_status[c / G];
-}
-
-struct ModelArgs {
-    const double* mu;
-    const double* q64;
-    double* mu_out;
-    double* q_out;
-    int cols, B;
-};
-
-__global__ void k_column_model(ModelArgs a) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (a.mu_out && i < a.cols * a.B) a.mu_out[i] = a.mu[i];
-    if (a.q_out && i < a.cols) a.q_out[i] = a.q64[i];
 }
 
 }  // namespace smf

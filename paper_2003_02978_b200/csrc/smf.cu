@@ -36,6 +36,8 @@ struct smf_ctx {
     int group = 1;    // detector columns per partition (smf_set_grouping)
     int mask = 0;     // nodata masking (smf_set_nodata)
     float nodata = -9999.f;
+    int lit_mode = SMF_COVCHECK_AUTO;   // literal covariance check (smf_set_covariance_check)
+    int diag = 0;                       // per-iteration diagnostics (smf_set_diagnostics)
     int last_launches = 0;
     char err[512] = {0};
     // profiling (smf_profile_*): events bracketing each launch
@@ -142,8 +144,10 @@ struct Plan {
     size_t smem1, smem2, smem3;
     // workspace offsets
     size_t o_mbar, o_mu, o_tprev, o_yprev, o_ainv, o_q64, o_z32, o_mhat, o_kc, o_q32, o_status, o_pilot, o_ghat, o_part1,
-        o_part3, o_tra, o_rho, o_tq, o_energy, o_nvalid, total;
+        o_part3, o_tra, o_rho, o_tq, o_energy, o_nvalid, o_nlit, o_lit, o_dnnz, o_dq, o_dst, o_dlit, total;
+    long long lit_stride;   // doubles per column of the wide literal-check scratch
     int n_energy;   // energy rows (n_iter + 1) or 0
+    int n_diag;     // diagnostics rows (n_iter + 1) or 0
 };
 
 int sweep_blocks_per_sm(int B);
@@ -243,6 +247,20 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.o_nvalid = take((size_t)cols * 8);
     p.n_energy = ctx->energy ? ctx->n_iter + 1 : 0;
     p.o_energy = take((size_t)std::max(p.n_energy, 1) * cols * 8);
+    p.o_nlit = take((size_t)cols * 4);
+    // wide literal covariance check (reading C16''): per-column fp64 scratch, aliased onto the
+    // K1w partials (dead once k2w_init has consumed them) when they are large enough
+    p.lit_stride = p.wide ? lit_doubles(B) : 0;
+    const size_t part1_bytes = p.wide ? (p.widetc ? (size_t)cols * bep * bep * 8 : (size_t)cols * p.NGw * kWideNT1 * 64 * 8)
+                                      : 0;
+    const size_t lit_bytes = (size_t)cols * p.lit_stride * 8;
+    p.o_lit = !p.wide ? 0 : (lit_bytes <= part1_bytes ? p.o_part1 : take(lit_bytes));
+    p.n_diag = ctx->diag ? ctx->n_iter + 1 : 0;
+    const size_t nd = (size_t)std::max(p.n_diag, 1) * cols;
+    p.o_dnnz = take(nd * 8);
+    p.o_dq = take(nd * 8);
+    p.o_dst = take(nd * 4);
+    p.o_dlit = take(nd * 4);
     p.total = o;
     return true;
 }
@@ -530,6 +548,7 @@ ColState col_state(const Plan& p, unsigned char* ws, const float* s, const smf_c
     cs.rho64 = (double*)(ws + p.o_rho);
     cs.tq = (double*)(ws + p.o_tq);
     cs.nvalid = (double*)(ws + p.o_nvalid);
+    cs.nlit = (int*)(ws + p.o_nlit);
     cs.mask = ctx->mask;
     cs.nodata = ctx->nodata;
     return cs;
@@ -545,8 +564,10 @@ smf_status validate(smf_ctx* ctx, const void* rad, int cols, int pixels, const v
         set_err(ctx, "absorption spectrum not set (smf_set_absorption)");
         return SMF_ERR_NOT_CONFIGURED;
     }
-    if (((uintptr_t)rad & 15) || ((uintptr_t)ws & 255)) {
-        set_err(ctx, "radiance must be 16-byte and workspace 256-byte aligned");
+    // the narrow path reads the cube through TMA tensor maps (16-byte aligned base); the wide
+    // path handles any float-aligned cube (per-row cp.async when the rows are not 16-byte runs)
+    if ((((uintptr_t)rad & 15) && narrow(ctx->bands)) || ((uintptr_t)rad & 3) || ((uintptr_t)ws & 255)) {
+        set_err(ctx, "radiance must be 16-byte (narrow path) / 4-byte (wide path) and workspace 256-byte aligned");
         return SMF_ERR_INVALID_ARGUMENT;
     }
     if (!g_encode) {
@@ -934,6 +955,65 @@ smf_status smf_energy_trace(smf_ctx* ctx, const void* workspace, int cols, int p
     return SMF_OK;
 }
 
+smf_status smf_set_covariance_check(smf_ctx* ctx, int mode) {
+    if (!ctx || mode < SMF_COVCHECK_OFF || mode > SMF_COVCHECK_ALWAYS) return SMF_ERR_INVALID_ARGUMENT;
+    ++ctx->gen;
+    ctx->lit_mode = mode;
+    return SMF_OK;
+}
+
+smf_status smf_set_diagnostics(smf_ctx* ctx, int enable) {
+    if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    ++ctx->gen;
+    ctx->diag = enable ? 1 : 0;
+    return SMF_OK;
+}
+
+// Copy a per-partition record array [rows][plan cols] (offset `which` of each plan) of the last
+// retrieve into dst [rows][partitions], following the grouping layout (full groups, remainder).
+static cudaError_t copy_records(smf_ctx* ctx, const unsigned char* ws, int cols, int pixels, size_t Plan::*which,
+                                int rows, size_t elem, void* dst, cudaStream_t st) {
+    if (!dst) return cudaSuccess;
+    GroupLayout g = GroupLayout::make(cols, ctx->group);
+    if (g.G == 1) {
+        Plan p;
+        make_plan(ctx, cols, pixels, p);
+        return cudaMemcpyAsync(dst, ws + p.*which, (size_t)rows * cols * elem, cudaMemcpyDeviceToDevice, st);
+    }
+    g.bytes(ctx, pixels);
+    smf_ctx tmp = *ctx;
+    tmp.group = 1;
+    Plan pf;
+    make_plan(&tmp, g.nfull, g.G * pixels, pf);
+    cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)g.parts * elem, ws + g.o_full + pf.*which, (size_t)g.nfull * elem,
+                                      (size_t)g.nfull * elem, rows, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess && g.rem > 0) {
+        Plan pr;
+        make_plan(&tmp, 1, g.rem * pixels, pr);
+        e = cudaMemcpy2DAsync((unsigned char*)dst + (size_t)g.nfull * elem, (size_t)g.parts * elem,
+                              ws + g.o_rem + pr.*which, elem, elem, rows, cudaMemcpyDeviceToDevice, st);
+    }
+    return e;
+}
+
+smf_status smf_iteration_diagnostics(smf_ctx* ctx, const void* workspace, int cols, int pixels, int64_t* nnz_out,
+                                     double* q_out, int32_t* status_out, int32_t* literal_out, void* stream) {
+    if (!ctx || !workspace || cols < 1 || pixels < 2) return SMF_ERR_INVALID_ARGUMENT;
+    if (!ctx->diag) {
+        set_err(ctx, "diagnostics not enabled (smf_set_diagnostics)");
+        return SMF_ERR_NOT_CONFIGURED;
+    }
+    const unsigned char* ws = (const unsigned char*)workspace;
+    const int rows = ctx->n_iter + 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = copy_records(ctx, ws, cols, pixels, &Plan::o_dnnz, rows, 8, nnz_out, st);
+    if (e == cudaSuccess) e = copy_records(ctx, ws, cols, pixels, &Plan::o_dq, rows, 8, q_out, st);
+    if (e == cudaSuccess) e = copy_records(ctx, ws, cols, pixels, &Plan::o_dst, rows, 4, status_out, st);
+    if (e == cudaSuccess) e = copy_records(ctx, ws, cols, pixels, &Plan::o_dlit, rows, 4, literal_out, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "iteration_diagnostics copy");
+    return SMF_OK;
+}
+
 smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind) {
     if (!ctx || kind < SMF_STATS_AUTO || kind > SMF_STATS_TENSOR) return SMF_ERR_INVALID_ARGUMENT;
     ++ctx->gen;
@@ -1095,6 +1175,23 @@ static smf_status retrieve_eager(smf_ctx* ctx, const float* radiance, int cols, 
     ua.G = p.G;
     ua.S = p.S;
     ua.ttot = p.ttot;
+    ua.L = radiance;
+    ua.enh = enhancement;
+    ua.alb = albedo;
+    ua.lit = (double*)(ws + p.o_lit);
+    ua.lit_stride = p.lit_stride;
+    ua.r_floor = (float)ctx->r_floor;
+    ua.use_albedo = ctx->use_albedo;
+    ua.lit_mode = ctx->lit_mode;
+    DiagArgs da;
+    da.enh = enhancement;
+    da.cs = cs;
+    da.nnz = (long long*)(ws + p.o_dnnz);
+    da.q = (double*)(ws + p.o_dq);
+    da.st = (int*)(ws + p.o_dst);
+    da.lit = (int*)(ws + p.o_dlit);
+    da.cols = cols;
+    da.N = pixels;
     const size_t smem_up = p.wide ? k2w_update_smem(p.B) : (size_t)p.B * p.B * 8;
     void* ufn = p.wide ? reinterpret_cast<void*>(&k2w_update) : reinterpret_cast<void*>(&k2_update);
     cudaError_t e0 = cudaFuncSetAttribute(ufn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_up);
@@ -1141,6 +1238,13 @@ static smf_status retrieve_eager(smf_ctx* ctx, const float* radiance, int cols, 
             k_energy<<<(cols + 127) / 128, 128, 0, st>>>(ua);
             e = cudaGetLastError();
             if (e != cudaSuccess) return cuda_fail(ctx, e, "k_energy launch");
+            ++launches;
+        }
+        if (ctx->diag) {   // per-iteration nonzero count, q^k, status, literal checks
+            da.k = k;
+            k_diag<<<cols, 256, 0, st>>>(da);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "k_diag launch");
             ++launches;
         }
     }
@@ -1329,19 +1433,11 @@ smf_status smf_retrieve_host(smf_ctx* ctx, const float* radiance_host, int cols,
 smf_status smf_column_model(smf_ctx* ctx, const void* workspace, int cols, int pixels, double* mu_out,
                             double* q_out, void* stream) {
     if (!ctx || !workspace || cols < 1 || pixels < 2) return SMF_ERR_INVALID_ARGUMENT;
-    Plan p;
-    make_plan(ctx, cols, pixels, p);
+    // per partition (the grouping layout resolved as for the energy trace): mu [parts][B], q [parts]
     const unsigned char* ws = (const unsigned char*)workspace;
-    ModelArgs a;
-    a.mu = (const double*)(ws + p.o_mu);
-    a.q64 = (const double*)(ws + p.o_q64);
-    a.mu_out = mu_out;
-    a.q_out = q_out;
-    a.cols = cols;
-    a.B = p.B;
-    int n = cols * p.B;
-    k_column_model<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(a);
-    cudaError_t e = cudaGetLastError();
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = copy_records(ctx, ws, cols, pixels, &Plan::o_mu, 1, (size_t)ctx->bands * 8, mu_out, st);
+    if (e == cudaSuccess) e = copy_records(ctx, ws, cols, pixels, &Plan::o_q64, 1, 8, q_out, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "column_model");
     return SMF_OK;
 }

@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
         a.cs.kc32[2 * c] = (float)qc[1];
         a.cs.kc32[2 * c + 1] = (float)qc[2];
         a.cs.status[c] = st;
+        a.cs.nlit[c] = 0;
     }
     // tr((C0 + rho I)^-1) for the energy trace (fixed order)
     double tl[1] = {0.0};
@@ -476,6 +477,9 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
 
 // ---------------------------------------------------------------- K2w update
 __host__ inline size_t k2w_update_smem(int B) { return (size_t)(2 * B + 32 * 18) * 8; }
+constexpr int kLitRows = 32;   // residual rows per chunk of the wide literal check
+// doubles of global scratch per column for the wide literal check (packed C^k + residual rows)
+__host__ inline long long lit_doubles(int B) { return (long long)B * (B + 1) / 2 + (long long)kLitRows * B; }
 
 __global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
     extern __shared__ double w3_smem[];
@@ -484,7 +488,7 @@ __global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
     double* sh_h = sh_t + B;       // [B]
     double* scratch = sh_h + B;    // [32][18]
     __shared__ double sh_coef[3], sh_s[3];
-    __shared__ int sh_st;
+    __shared__ int sh_st, sh_lit;
     ColState& cs = a.cs;
     if (cs.status[c] != COL_OK) return;   // uniform per block
     const double* Ainv = cs.ainv + (size_t)c * B * B;
@@ -583,16 +587,28 @@ __global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
             v[i] = gv[i * 3 + 1];
         }
         int st = COL_OK;
-        if (!solve3(K, v, x)) st = COL_NOT_SPD;
+        const bool solved = solve3(K, v, x);
+        if (!solved) st = COL_NOT_SPD;
         for (int i = 0; i < 3; ++i) {
             double s2 = 0.0;
             for (int l = 0; l < 3; ++l) s2 += M[i][l] * x[l];
             sh_coef[i] = s2;
         }
         sh_st = st;
+        sh_lit = a.lit_mode == 2 || (a.lit_mode == 1 && (!solved || !(min_eig3(K) > kLitTau)));
         if (a.energy_on) cs.tq[c] = woodbury_trace(M, gv, gv + 9, B, cs.rho64[c], cs.tra[c], bbar);
     }
     __syncthreads();
+    if (sh_lit) {
+        // lines 10-16 literally (reading C16''), C^k and the residual rows in global scratch
+        double* Cp = a.lit + (size_t)c * a.lit_stride;
+        const int stl = literal_iteration(a, c, Ainv, Cp, Cp + (size_t)B * (B + 1) / 2, kLitRows, w3_smem, scratch);
+        if (tid == 0) {
+            cs.status[c] = stl;
+            cs.nlit[c] += 1;
+        }
+        return;
+    }
     // 4. z = y_t - Y M (I + G M)^-1 U^T A^-1 t (Woodbury), q, mhat.z, mu.z
     double qc[3] = {0.0, 0.0, 0.0};
 #pragma unroll

@@ -49,6 +49,9 @@ SYMBOLS = {
     "smf_stats_kernel_used": (_i, [_vp]),
     "smf_host_chunk_cols": (_i, [_vp, _i, ctypes.POINTER(_i)]),
     "smf_set_graph": (_i, [_vp, _i]),
+    "smf_set_covariance_check": (_i, [_vp, _i]),
+    "smf_set_diagnostics": (_i, [_vp, _i]),
+    "smf_iteration_diagnostics": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "smf_profile_enable": (_i, [_vp, _i]),
     "smf_profile_read": (_i, [_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_i)]),
     "smf_status_string": (ctypes.c_char_p, [_i]),
@@ -113,13 +116,24 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def _record(tensors, stream, device):
+    """Tensors allocated on torch's current stream but used by kernels on `stream`: tell
+    the caching allocator, so their memory is not handed out again before `stream` is done."""
+    import torch
+    if stream != torch.cuda.current_stream(device):
+        for t in tensors:
+            t.record_stream(stream)
+
+
 class Retriever:
     """A library context (smf_ctx) bound to the current CUDA device."""
 
     STATS_KERNELS = {"auto": 0, "ffma": 1, "tensor": 2}
+    COV_CHECKS = {"off": 0, "auto": 1, "always": 2}
 
     def __init__(self, bands, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2, ridge_rel=0.0,
-                 r_floor=0.05, stats_kernel="auto", energy=False, group=1, nodata=None, graph=False):
+                 r_floor=0.05, stats_kernel="auto", energy=False, group=1, nodata=None, graph=False,
+                 cov_check="auto", diagnostics=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("smf needs a CUDA device (no CPU fallback)")
@@ -137,6 +151,8 @@ class Retriever:
         self._check(_lib.smf_set_nodata(self._h, int(nodata is not None),
                                         float(nodata) if nodata is not None else -9999.0))
         self._check(_lib.smf_set_graph(self._h, int(bool(graph))))
+        self._check(_lib.smf_set_covariance_check(self._h, self.COV_CHECKS[cov_check]))
+        self._check(_lib.smf_set_diagnostics(self._h, int(bool(diagnostics))))
         self.group = int(group)
         self.n_iter = int(n_iter)
 
@@ -150,6 +166,24 @@ class Retriever:
         st = stream if stream is not None else torch.cuda.current_stream(workspace.device)
         self._check(_lib.smf_energy_trace(self._h, _ptr(workspace), cols, pixels, _ptr(out),
                                           ctypes.c_void_p(st.cuda_stream)))
+        return out
+
+    def iteration_diagnostics(self, workspace, cols, pixels, stream=None):
+        """Per-iteration records of the last retrieve that used `workspace` (requires
+        diagnostics=True), each [n_iter + 1][partitions]: nonzero count of alpha^k (int64),
+        q^k (fp64), partition status (int32), cumulative literal covariance checks (int32)."""
+        import torch
+        nparts = len(group_partitions(cols, self.group))
+        dev = workspace.device
+        shape = (self.n_iter + 1, nparts)
+        out = {"nnz": torch.empty(shape, dtype=torch.int64, device=dev),
+               "q": torch.empty(shape, dtype=torch.float64, device=dev),
+               "status": torch.empty(shape, dtype=torch.int32, device=dev),
+               "literal": torch.empty(shape, dtype=torch.int32, device=dev)}
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        self._check(_lib.smf_iteration_diagnostics(self._h, _ptr(workspace), cols, pixels, _ptr(out["nnz"]),
+                                                   _ptr(out["q"]), _ptr(out["status"]), _ptr(out["literal"]),
+                                                   ctypes.c_void_p(st.cuda_stream)))
         return out
 
     @property
@@ -208,15 +242,21 @@ class Retriever:
         if bands != self.bands:
             raise SMFError(SMF_ERR_SHAPE, f"bands {bands} != {self.bands}")
         dev = radiance.device
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        made = []   # allocated here on torch's current stream but used on `st`
         if enhancement is None:
             enhancement = torch.empty((cols, pixels), dtype=torch.float32, device=dev)
+            made.append(enhancement)
         if albedo is None:
             albedo = torch.empty((cols, pixels), dtype=torch.float32, device=dev)
+            made.append(albedo)
         if workspace is None:
             workspace = self.alloc_workspace(cols, pixels, dev)
+            made.append(workspace)
         if status is None:
             status = torch.empty(cols, dtype=torch.int32, device=dev)
-        st = stream if stream is not None else torch.cuda.current_stream(dev)
+            made.append(status)
+        _record(made, st, dev)
         self._check(_lib.smf_retrieve(self._h, _ptr(radiance), cols, pixels, _ptr(enhancement), _ptr(albedo),
                                       _ptr(workspace), _ptr(status), ctypes.c_void_p(st.cuda_stream)))
         return enhancement, albedo, status
@@ -270,18 +310,23 @@ class Retriever:
         cols, pixels, bands = radiance.shape
         mean = torch.empty((cols, bands), dtype=torch.float64, device=radiance.device)
         cov = torch.empty((cols, bands, bands), dtype=torch.float64, device=radiance.device)
+        st = stream if stream is not None else torch.cuda.current_stream(radiance.device)
+        made = [mean, cov]
         if workspace is None:
             workspace = self.alloc_workspace(cols, pixels, radiance.device)
-        st = stream if stream is not None else torch.cuda.current_stream(radiance.device)
+            made.append(workspace)
+        _record(made, st, radiance.device)
         self._check(_lib.smf_initial_statistics(self._h, _ptr(radiance), cols, pixels, _ptr(mean), _ptr(cov),
                                                 _ptr(workspace), ctypes.c_void_p(st.cuda_stream)))
         return mean, cov
 
     def column_model(self, workspace, cols, pixels, stream=None):
-        """mu^{N_iter} (fp64 [cols][bands]) and q^{N_iter} (fp64 [cols]) of the last retrieve."""
+        """mu^{N_iter} (fp64 [partitions][bands]) and q^{N_iter} (fp64 [partitions]) of the last
+        retrieve (one partition per column unless grouped)."""
         import torch
-        mu = torch.empty((cols, self.bands), dtype=torch.float64, device=workspace.device)
-        q = torch.empty(cols, dtype=torch.float64, device=workspace.device)
+        nparts = len(group_partitions(cols, self.group))
+        mu = torch.empty((nparts, self.bands), dtype=torch.float64, device=workspace.device)
+        q = torch.empty(nparts, dtype=torch.float64, device=workspace.device)
         st = stream if stream is not None else torch.cuda.current_stream(workspace.device)
         self._check(_lib.smf_column_model(self._h, _ptr(workspace), cols, pixels, _ptr(mu), _ptr(q),
                                           ctypes.c_void_p(st.cuda_stream)))
