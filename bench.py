@@ -6,8 +6,10 @@
 
 One step = one smf_retrieve of the whole flightline (K1 stats, K2 init, 31 sweeps,
 30 column updates) on inputs resident in HBM (3.44 GB > 126 MB L2, so no flush is
-needed between steps). Multi-GPU (torchrun): every rank retrieves its own
-flightline (independent units, no collective), "scaling": "weak".
+needed between steps). Multi-GPU (torchrun): `--split columns` (default) shards the
+flightline's detector columns over the ranks (independent partitions; no
+collective), "scaling": "strong"; `--split replicas` gives every rank its own
+flightline, "scaling": "weak".
 `--impl reference` times the fp64 CPU oracle (the only reference this paper has)
 on a bounded sample of the same workload on the host cores.
 """
@@ -41,7 +43,20 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-cols", type=int, default=None)
+    ap.add_argument("--stats-kernel", default="auto", choices=["auto", "ffma", "tensor"],
+                    help="initial-statistics kernel (A/B measurement; auto = the library default)")
+    ap.add_argument("--split", default="columns", choices=["columns", "replicas"],
+                    help="N > 1: shard one flightline's columns (strong) or one flightline per rank (weak)")
     return ap.parse_args()
+
+
+L2_BYTES = 126 << 20
+
+
+def metric_for(cfg):
+    if cfg.name == "flightline":
+        return METRIC
+    return f"pixel·iterations/sec ({cfg.cols}×{cfg.pixels}×{cfg.bands} fp32) and % of binding roofline"
 
 
 def dist_env():
@@ -74,6 +89,12 @@ def load_scene(cfg, rank, world):
         return np.load(key + ".npy", mmap_mode="r"), synth.unit_absorption(cfg)
     cube, s, _ = synth.generate(cfg)
     return cube, s
+
+
+def oracle_column_seconds(cfg, n_iter):
+    """Estimated single-thread oracle time per column (35 ms per column-iteration at
+    N = 20000, B = 72; the covariance loop is N B^2)."""
+    return 0.035 * (cfg.pixels / 20000) * (cfg.bands / 72) ** 2 * (n_iter + 1)
 
 
 class ClockSampler:
@@ -145,9 +166,10 @@ def cpu_baseline(cfg, cube, s, n_iter, sample_cols=None, impl_note="oracle"):
     import oracle
     threads = oracle.max_threads()
     if sample_cols is None:
-        # ~1 s of oracle work per core-column at N = 20000, B = 72 (35 ms / column-iteration):
-        # 16 columns per thread -> ~15 s of CPU work (bounded sample)
-        sample_cols = max(1, min(cfg.cols, 16 * threads))
+        # ~15 s of CPU work in total (bounded sample): at N = 20000, B = 72 a
+        # column is ~1 s of oracle work, so 16 columns per thread
+        per_thread = max(1, int(15.0 / oracle_column_seconds(cfg, n_iter)))
+        sample_cols = max(1, min(cfg.cols, per_thread * threads))
     cols = np.linspace(0, cfg.cols - 1, sample_cols).astype(int)
     sub = np.ascontiguousarray(cube[cols])
     t0 = time.perf_counter()
@@ -168,8 +190,9 @@ def run_reference(args, cfg):
     import oracle
     oracle.build()
     threads = oracle.max_threads()
-    # each reference step: 2 columns per host thread (~2 s), so K + W steps end in minutes
-    sample = args.cpu_sample_cols or max(1, min(cfg.cols, 2 * threads))
+    # each reference step: ~2 s of oracle work per host thread, so K + W steps end in minutes
+    per_thread = max(1, int(2.0 / oracle_column_seconds(cfg, cfg.n_iter)))
+    sample = args.cpu_sample_cols or max(1, min(cfg.cols, per_thread * threads))
     for _ in range(args.warmup):
         cpu_baseline(cfg, cube, s, cfg.n_iter, sample)
     vals = []
@@ -180,10 +203,10 @@ def run_reference(args, cfg):
         t_all += time.perf_counter() - t0
         vals.append(cb["value"])
     value = float(statistics.median(vals))
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": metric_for(cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(cfg, args.gpus),
+            "data": "synthetic", "config": workload_config(cfg, args.gpus, args.split),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                              "sample": cb["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -191,13 +214,23 @@ def run_reference(args, cfg):
     return 0
 
 
-def workload_config(cfg, n_gpus):
+def needs_flush(cube_bytes):
+    return cube_bytes <= 2 * L2_BYTES
+
+
+def workload_config(cfg, n_gpus, split="columns"):
+    per_rank = cfg.cube_bytes if (n_gpus == 1 or split == "replicas") else cfg.cube_bytes / n_gpus
+    gb = per_rank / 1e9
+    if needs_flush(per_rank):
+        l2 = (f"inputs {gb:.3f} GB per rank <= 2x the 126 MB L2: a 256 MB L2 flush between steps, "
+              f"outside the timed events (per-step event pairs)")
+    else:
+        l2 = f"inputs {gb:.2f} GB per rank > 2x the 126 MB L2 (no flush needed)"
+    par = "single-gpu" if n_gpus == 1 else (f"columns/{n_gpus}" if split == "columns" else "replicas")
     return {"workload": f"{cfg.name} {cfg.cols}x{cfg.pixels}x{cfg.bands} fp32, {cfg.n_iter} IRL1 iterations, "
                         f"sparsity+albedo on",
             "cols": cfg.cols, "pixels": cfg.pixels, "bands": cfg.bands, "n_iter": cfg.n_iter,
-            "l2": "inputs 3.44 GB per rank >> 126 MB L2 (no flush needed)" if cfg.cube_bytes > 1e9 else
-                  "inputs smaller than L2; L2 flushed between steps",
-            "parallelism": "replicas" if n_gpus > 1 else "single-gpu"}
+            "l2": l2, "parallelism": par}
 
 
 def run_campaign(args):
@@ -279,31 +312,44 @@ def main():
 
     rank, world, local = dist_env()
     import torch
+    # one process per GPU; with fewer visible GPUs than ranks (a plumbing test on one GPU,
+    # never a measurement) ranks share devices round-robin and talk over gloo
+    ndev = torch.cuda.device_count()
+    local = local if local < ndev else local % ndev
+    shared = world > ndev
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import __graft_entry__
     if rank == 0:
         __graft_entry__.build()
     if world > 1:
         torch.distributed.barrier()
-    from paper_2003_02978_b200 import smf
+    from paper_2003_02978_b200 import shard, smf
 
+    split = args.split if world > 1 else "columns"
     cube, s = load_scene(cfg, rank, world)
+    # this rank's detector columns: a contiguous slice of the flightline (columns are
+    # independent partitions; no collective on the data path), or the whole
+    # flightline per rank for --split replicas
+    c0, c1 = shard.column_range(cfg.cols, rank, world) if split == "columns" else (0, cfg.cols)
+    ncols = c1 - c0
     dev = torch.device("cuda", local)
-    rad = torch.from_numpy(np.ascontiguousarray(cube)).to(dev)
-    r = smf.Retriever(cfg.bands, s, n_iter=cfg.n_iter)
-    ws = r.alloc_workspace(cfg.cols, cfg.pixels, dev)
-    enh = torch.empty((cfg.cols, cfg.pixels), dtype=torch.float32, device=dev)
+    rad = torch.from_numpy(np.ascontiguousarray(cube[c0:c1])).to(dev)
+    r = smf.Retriever(cfg.bands, s, n_iter=cfg.n_iter, stats_kernel=args.stats_kernel)
+    ws = r.alloc_workspace(ncols, cfg.pixels, dev)
+    enh = torch.empty((ncols, cfg.pixels), dtype=torch.float32, device=dev)
     alb = torch.empty_like(enh)
-    st = torch.empty(cfg.cols, dtype=torch.int32, device=dev)
+    st = torch.empty(ncols, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    l2_flush = None if cfg.cube_bytes > 1e9 else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    rank_bytes = ncols * cfg.pixels * cfg.bands * 4
+    l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if needs_flush(rank_bytes) else None
 
     def step():
-        if l2_flush is not None:
-            l2_flush.zero_()
         r.retrieve(rad, enh, alb, ws, st, stream)
 
     for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
@@ -311,87 +357,105 @@ def main():
     torch.cuda.synchronize()
     first_fail = r.synchronize(st)
     if first_fail >= 0:
-        raise SystemExit(f"column {first_fail} failed")
+        raise SystemExit(f"column {c0 + first_fail} failed")
 
-    # ---- timed region (device time, CUDA events on the launching stream)
+    def timed_steps():
+        """Device time of K steps (ms). Inputs > 2x L2: one event pair around the K steps.
+        Smaller inputs: an L2 flush before every step, outside per-step event pairs."""
+        if l2_flush is None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1)
+        evs = []
+        for _ in range(args.steps):
+            l2_flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs)
+
+    # ---- timed region (device time, CUDA events on the launching stream, max over ranks)
     prof_in_timed = os.environ.get("SMF_BENCH_PROF", "0") != "0"
     r.profile_enable(prof_in_timed)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
+        ms = timed_steps()
     if world > 1:
         torch.distributed.barrier()
-    ms = ev0.elapsed_time(ev1)
     if not prof_in_timed:
         # per-kernel event brackets break the programmatic-dependent-launch overlap of
         # consecutive kernels, so the kernel durations come from a second, bracketed pass
         # of the same K steps right after the timed region
         r.profile_enable(True)
-        for _ in range(args.steps):
-            step()
-        torch.cuda.synchronize()
+        timed_steps()
     prof = r.profile_read()
     r.profile_enable(False)
     launches_per_step = r.last_launch_count
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms], dtype=torch.float64, device="cpu" if shared else dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    units_per_step = cfg.cols * cfg.pixels * cfg.n_iter * world
+    job_cols = cfg.cols if split == "columns" else cfg.cols * world
+    units_per_step = job_cols * cfg.pixels * cfg.n_iter
     value = units_per_step / (ms_per_step * 1e-3)
 
-    # ---- roofline of the dominant kernel (K3 sweep), measured live
+    # ---- roofline of the dominant kernel (the sweep), measured live on this rank's share
     peak, peak_src = peaks()
-    total_bytes, sweep_bytes = algorithmic_bytes(cfg, cfg.n_iter, True)
+    rcfg = synth.scaled(cfg, cols=ncols)
+    total_bytes, sweep_bytes = algorithmic_bytes(rcfg, cfg.n_iter, True)
     k3_ms, k3_n = prof["k3_sweep"]
     k3_avg_s = k3_ms * 1e-3 / max(k3_n, 1)
     k3_bytes_avg = sum(sweep_bytes) / len(sweep_bytes)
     achieved = k3_bytes_avg / k3_avg_s / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and ncols == cfg.cols:
         try:
-            traffic = json.load(open(tpath)).get(cfg.name, {}).get("k3_sweep")
+            ent = json.load(open(tpath)).get(cfg.name, {})
+            traffic, traffic_src = ent.get("k3_sweep"), ent.get("source")
         except Exception:
             traffic = None
-    step_achieved = total_bytes / (ms_per_step * 1e-3) / 1e9 * 1.0
+    step_achieved = total_bytes / (ms_per_step * 1e-3) / 1e9
     kernel_share = {k: (v[0] / max(sum(x[0] for x in prof.values()), 1e-9)) for k, v in prof.items()}
 
     # ---- end to end through the public API with host buffers (pinned)
     e2e = None
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(args.steps, 10))
     if e2e_steps > 0:
-        h_rad = torch.from_numpy(np.ascontiguousarray(cube)).pin_memory()
-        h_enh = torch.empty((cfg.cols, cfg.pixels), dtype=torch.float32).pin_memory()
+        h_rad = torch.from_numpy(np.ascontiguousarray(cube[c0:c1])).pin_memory()
+        h_enh = torch.empty((ncols, cfg.pixels), dtype=torch.float32).pin_memory()
         h_alb = torch.empty_like(h_enh).pin_memory()
-        h_st = torch.empty(cfg.cols, dtype=torch.int32).pin_memory()
+        h_st = torch.empty(ncols, dtype=torch.int32).pin_memory()
         r2 = smf.Retriever(cfg.bands, s, n_iter=cfg.n_iter)
-        rc = r2.retrieve_host_ptr(h_rad.data_ptr(), cfg.cols, cfg.pixels, h_enh.data_ptr(), h_alb.data_ptr(),
+        rc = r2.retrieve_host_ptr(h_rad.data_ptr(), ncols, cfg.pixels, h_enh.data_ptr(), h_alb.data_ptr(),
                                   h_st.data_ptr())   # warm-up (allocates the context buffers)
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            rc = r2.retrieve_host_ptr(h_rad.data_ptr(), cfg.cols, cfg.pixels, h_enh.data_ptr(),
+            rc = r2.retrieve_host_ptr(h_rad.data_ptr(), ncols, cfg.pixels, h_enh.data_ptr(),
                                       h_alb.data_ptr(), h_st.data_ptr())
         dt = (time.perf_counter() - t0) / e2e_steps
         if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             dt = float(t.item())
+        nb = world if split == "replicas" else 1
         e2e = {"value": units_per_step / dt, "unit": UNIT,
-               "h2d_bytes_per_step": int(h_rad.numel() * 4),
-               "d2h_bytes_per_step": int((h_enh.numel() + h_alb.numel() + h_st.numel()) * 4),
+               "h2d_bytes_per_step": int(cfg.cube_bytes * nb),
+               "d2h_bytes_per_step": int((2 * cfg.cols * cfg.pixels + cfg.cols) * 4 * nb),
                "ms_per_step": dt * 1e3, "rc": rc,
-               "bound_note": "PCIe H2D of the 3.44 GB cube dominates (cf. the paper's I/O-bound campaign, P:790)"}
+               "bound_note": "PCIe H2D of the cube dominates (cf. the paper's I/O-bound campaign, P:790)"}
         del r2
 
     cpu = None
@@ -402,12 +466,15 @@ def main():
             cpu = {"error": str(ex)}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        line = {"metric": metric_for(cfg), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong" if (world > 1 and split == "columns") else "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": workload_config(cfg, world),
-                "roofline": {"bound": "hbm", "kernel": "k3_sweep", "achieved": achieved, "peak": peak,
+                "config": workload_config(cfg, world, split),
+                "roofline": {"bound": "hbm", "kernel": "k3_sweep" if cfg.bands <= 96 and cfg.bands % 4 == 0
+                             else "k3w_sweep", "achieved": achieved, "peak": peak,
                              "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                             "traffic_source": traffic_src,
                              "algorithmic_bytes_per_launch": k3_bytes_avg, "launches": k3_n,
                              "avg_launch_us": k3_avg_s * 1e6, "peak_source": peak_src,
                              "step_achieved_gbs": step_achieved, "step_frac": step_achieved / peak,
@@ -417,10 +484,13 @@ def main():
                              "kernel_durations": "CUDA events bracketing each launch on its stream, "
                                                  + ("inside the timed region" if prof_in_timed else
                                                     "in a second pass of the same K steps right after "
-                                                    "the (unbracketed) timed region")},
+                                                    "the (unbracketed) timed region")
+                                                 + (f"; rank 0's {ncols}-column share" if world > 1 else "")},
                 "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk.summary(),
                 "gpu_launches": launches_per_step * args.steps}
+        if shared:
+            line["note"] = f"{world} ranks on {ndev} GPU(s): plumbing test, not a measurement"
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

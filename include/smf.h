@@ -198,8 +198,8 @@ smf_status smf_set_nodata(smf_ctx* ctx, int enable, float value);
  * detector columns = cols, lines = along-track pixels):
  *   SMF_LAYOUT_BIL: in [lines][bands][samples] (band interleaved by line);
  *   SMF_LAYOUT_BIP: in [lines][samples][bands] (band interleaved by pixel).
- * in, out: device fp32, caller-owned, must not overlap; enqueued on `stream`.
- * SMF_ERR_SHAPE if BIL has more than 65535 lines (grid limit). */
+ * in, out: device fp32, caller-owned, must not overlap; enqueued on `stream`. Any
+ * number of lines (the kernels grid-stride over lines). */
 enum { SMF_LAYOUT_BIL = 0, SMF_LAYOUT_BIP = 1 };
 smf_status smf_convert_layout(const float* in, int lines, int samples, int bands, int layout, float* out,
                               void* stream);
@@ -267,6 +267,12 @@ smf_status smf_set_covariance_check(smf_ctx* ctx, int mode);
 smf_status smf_set_diagnostics(smf_ctx* ctx, int enable);
 smf_status smf_iteration_diagnostics(smf_ctx* ctx, const void* workspace, int cols, int pixels, int64_t* nnz_out,
                                      double* q_out, int32_t* status_out, int32_t* literal_out, void* stream);
+
+/* NVTX ranges (enable != 0): every kernel enqueue of smf_retrieve is wrapped in an NVTX
+ * range named after its step (smf:stats / smf:init / smf:update / smf:sweep, with the
+ * algorithm lines it implements), for timeline tools. Default: off unless the environment
+ * variable SMF_NVTX=1 is set when the first range would be pushed. No effect on results. */
+smf_status smf_set_nvtx(smf_ctx* ctx, int enable);
 
 /* Kernel launches enqueued by the last smf_retrieve call on this context. */
 int smf_last_launch_count(const smf_ctx* ctx);

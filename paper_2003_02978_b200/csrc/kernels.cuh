@@ -1967,30 +1967,34 @@ namespace smf {
 // HBM-bound: one read and one write of the cube.
 __global__ void k_bip_to_cpb(const float* __restrict__ in, float* __restrict__ out, int lines, int samples,
                              int bands) {
-    // block (p, c0): a warp per sample row, lanes stride the bands
-    const int p = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int c = blockIdx.x * nw + w; c < samples; c += gridDim.x * nw) {
-        const float* src = in + ((size_t)p * samples + c) * bands;
-        float* dst = out + ((size_t)c * lines + p) * bands;
-        for (int b = lane; b < bands; b += 32) dst[b] = __ldg(src + b);
-    }
+    // block (c0, line group): a warp per sample row, lanes stride the bands; lines grid-stride
+    // over gridDim.y (no 65535-line limit)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int p = blockIdx.y; p < lines; p += gridDim.y)
+        for (int c = blockIdx.x * nw + w; c < samples; c += gridDim.x * nw) {
+            const float* src = in + ((size_t)p * samples + c) * bands;
+            float* dst = out + ((size_t)c * lines + p) * bands;
+            for (int b = lane; b < bands; b += 32) dst[b] = __ldg(src + b);
+        }
 }
 
 __global__ void k_bil_to_cpb(const float* __restrict__ in, float* __restrict__ out, int lines, int samples,
                              int bands) {
     __shared__ float tile[32][33];
-    const int p = blockIdx.z;
     const int c0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
-    const float* src = in + (size_t)p * bands * samples;
-    for (int j = ty; j < 32; j += 8) {
-        const int b = b0 + j, c = c0 + tx;
-        tile[j][tx] = (b < bands && c < samples) ? __ldg(src + (size_t)b * samples + c) : 0.f;
-    }
-    __syncthreads();
-    for (int j = ty; j < 32; j += 8) {
-        const int c = c0 + j, b = b0 + tx;
-        if (c < samples && b < bands) out[((size_t)c * lines + p) * bands + b] = tile[tx][j];
+    for (int p = blockIdx.z; p < lines; p += gridDim.z) {   // lines grid-stride over gridDim.z
+        const float* src = in + (size_t)p * bands * samples;
+        for (int j = ty; j < 32; j += 8) {
+            const int b = b0 + j, c = c0 + tx;
+            tile[j][tx] = (b < bands && c < samples) ? __ldg(src + (size_t)b * samples + c) : 0.f;
+        }
+        __syncthreads();
+        for (int j = ty; j < 32; j += 8) {
+            const int c = c0 + j, b = b0 + tx;
+            if (c < samples && b < bands) out[((size_t)c * lines + p) * bands + b] = tile[tx][j];
+        }
+        __syncthreads();
     }
 }
 }  // namespace smf

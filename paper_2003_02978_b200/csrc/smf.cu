@@ -17,6 +17,8 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3 (no-op unless a tool is attached)
+
 #include "../../include/smf.h"
 #include "kernels.cuh"
 #include "wide.cuh"
@@ -38,6 +40,7 @@ struct smf_ctx {
     float nodata = -9999.f;
     int lit_mode = SMF_COVCHECK_AUTO;   // literal covariance check (smf_set_covariance_check)
     int diag = 0;                       // per-iteration diagnostics (smf_set_diagnostics)
+    int nvtx = -1;                      // NVTX range per launch (smf_set_nvtx; -1: SMF_NVTX env)
     int last_launches = 0;
     char err[512] = {0};
     // profiling (smf_profile_*): events bracketing each launch
@@ -107,13 +110,35 @@ cudaEvent_t get_event(smf_ctx* ctx) {
     return e;
 }
 
-// Bracket one launch with events when profiling is on.
+bool nvtx_on(const smf_ctx* ctx) {
+    static const int env = [] {
+        const char* e = std::getenv("SMF_NVTX");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return ctx->nvtx < 0 ? env != 0 : ctx->nvtx != 0;
+}
+
+const char* kernel_kind_name(int kind) {
+    switch (kind) {
+        case SMF_KERNEL_STATS: return "smf:stats (K0/K1, Fig. alg lines 2-3)";
+        case SMF_KERNEL_INIT: return "smf:init (K2, lines 2-6)";
+        case SMF_KERNEL_UPDATE: return "smf:update (K2, lines 9-16)";
+        case SMF_KERNEL_SWEEP: return "smf:sweep (K3, lines 5, 9, 16)";
+    }
+    return "smf:other";
+}
+
+// Bracket one launch with events when profiling is on, and with an NVTX range when
+// NVTX is on (host-side range around the enqueue; tools map it to the launch).
 struct ProfScope {
     smf_ctx* ctx;
     cudaStream_t st;
     int kind;
     cudaEvent_t a = nullptr;
+    bool nv = false;
     ProfScope(smf_ctx* c, cudaStream_t s, int k) : ctx(c), st(s), kind(k) {
+        nv = nvtx_on(ctx);
+        if (nv) nvtxRangePushA(kernel_kind_name(kind));
         if (ctx->prof) {
             a = get_event(ctx);
             cudaEventRecord(a, st);
@@ -125,6 +150,7 @@ struct ProfScope {
             cudaEventRecord(b, st);
             ctx->recs.push_back({kind, a, b});
         }
+        if (nv) nvtxRangePop();
     }
 };
 
@@ -962,6 +988,12 @@ smf_status smf_set_covariance_check(smf_ctx* ctx, int mode) {
     return SMF_OK;
 }
 
+smf_status smf_set_nvtx(smf_ctx* ctx, int enable) {
+    if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
+    ctx->nvtx = enable ? 1 : 0;
+    return SMF_OK;
+}
+
 smf_status smf_set_diagnostics(smf_ctx* ctx, int enable) {
     if (!ctx) return SMF_ERR_INVALID_ARGUMENT;
     ++ctx->gen;
@@ -1039,11 +1071,10 @@ smf_status smf_convert_layout(const float* in, int lines, int samples, int bands
     cudaStream_t st = (cudaStream_t)stream;
     if (layout == SMF_LAYOUT_BIP) {
         const int warps = 8, gx = std::min((samples + warps - 1) / warps, 64);
-        k_bip_to_cpb<<<dim3(gx, lines), warps * 32, 0, st>>>(in, out, lines, samples, bands);
+        k_bip_to_cpb<<<dim3(gx, std::min(lines, 65535)), warps * 32, 0, st>>>(in, out, lines, samples, bands);
     } else {
-        if (lines > 65535) return SMF_ERR_SHAPE;
-        k_bil_to_cpb<<<dim3((samples + 31) / 32, (bands + 31) / 32, lines), dim3(32, 8), 0, st>>>(in, out, lines,
-                                                                                                samples, bands);
+        k_bil_to_cpb<<<dim3((samples + 31) / 32, (bands + 31) / 32, std::min(lines, 65535)), dim3(32, 8), 0, st>>>(
+            in, out, lines, samples, bands);
     }
     return cudaGetLastError() == cudaSuccess ? SMF_OK : SMF_ERR_CUDA;
 }

@@ -51,6 +51,7 @@ SYMBOLS = {
     "smf_set_graph": (_i, [_vp, _i]),
     "smf_set_covariance_check": (_i, [_vp, _i]),
     "smf_set_diagnostics": (_i, [_vp, _i]),
+    "smf_set_nvtx": (_i, [_vp, _i]),
     "smf_iteration_diagnostics": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "smf_profile_enable": (_i, [_vp, _i]),
     "smf_profile_read": (_i, [_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_i)]),
@@ -133,7 +134,7 @@ class Retriever:
 
     def __init__(self, bands, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2, ridge_rel=0.0,
                  r_floor=0.05, stats_kernel="auto", energy=False, group=1, nodata=None, graph=False,
-                 cov_check="auto", diagnostics=False):
+                 cov_check="auto", diagnostics=False, nvtx=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("smf needs a CUDA device (no CPU fallback)")
@@ -153,6 +154,8 @@ class Retriever:
         self._check(_lib.smf_set_graph(self._h, int(bool(graph))))
         self._check(_lib.smf_set_covariance_check(self._h, self.COV_CHECKS[cov_check]))
         self._check(_lib.smf_set_diagnostics(self._h, int(bool(diagnostics))))
+        if nvtx is not None:
+            self._check(_lib.smf_set_nvtx(self._h, int(bool(nvtx))))
         self.group = int(group)
         self.n_iter = int(n_iter)
 

@@ -42,3 +42,21 @@ def test_gpu_arm_json_contract():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 598 * 20000 * 72 * 4 and e["d2h_bytes_per_step"] > 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_multi_rank_plumbing():
+    """The N > 1 launch path (torchrun, --split columns): each rank retrieves its contiguous
+    column range of one flightline, the time is the max over ranks, rank 0 prints one line.
+    On a one-GPU box the two ranks share the device (gloo): checks the plumbing and the
+    contract keys only -- the number is not a measurement."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--config", "segment", "--steps", "2", "--warmup", "3", "--e2e-steps", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["parallelism"] == "columns/2"
+    assert d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 598 * 2000 * 72 * 4

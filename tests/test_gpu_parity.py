@@ -148,6 +148,7 @@ def test_flightline_full_size_sampled_columns(smf, torch):
         print(rep)
         assert rep["albedo_max_rel"] <= 1e-5
         assert abs(rep["q_rel"]) < 1e-4
+        assert rep["n_nan_mismatch"] == 0 and rep["zero_set_agreement"] > 0.999, rep
         if rep["n_bad"]:
             cls = c18_classify(enh[c], a_ref, cube[c], s,
                                lambda L, ss: oracle.retrieve_column(L, ss, n_iter=cfg.n_iter)[0], rep["tol"])
@@ -174,7 +175,8 @@ def test_ragged_shapes(smf, torch, cols, pixels, bands):
 
 # ------------------------------------------------------------------ wide path (any band count)
 @pytest.mark.parametrize("cols,pixels,bands", [(2, 300, 5), (3, 257, 13), (2, 700, 101), (1, 130, 98),
-                                               (2, 1200, 425), (2, 200, 1), (2, 200, 2), (1, 3000, 626)])
+                                               (2, 1200, 425), (2, 200, 1), (2, 200, 2), (1, 3000, 626),
+                                               (2, 400, 33), (2, 600, 127), (2, 2500, 250)])
 def test_wide_bands(smf, torch, cols, pixels, bands):
     """Band counts outside the narrow kernels (B % 4 != 0 or B > 96) run the wide path
     (k1w_stats / k2w_init / k2w_update / k3w_sweep)."""
@@ -204,18 +206,33 @@ def test_wide_initial_statistics(smf, torch, kernel):
         assert (np.abs(cov[c] - C_ref) / scale).max() < 1e-5
 
 
-def test_stress_columns_parity(smf, torch):
-    """BASELINE.json configs[3] (598 x 4000 x 425, 30 iterations): sampled columns,
-    including plume columns, against the oracle."""
-    cfg = synth.CONFIGS["stress"]
-    cols = _plume_columns(cfg, k=3, extra=2, seed=2)
-    cube, s, _ = synth.generate(cfg, columns=cols)
+@pytest.mark.parametrize("name", ["stress", "segment"])
+def test_full_size_config_sampled_columns(smf, torch, name):
+    """BASELINE.json configs[3] (598 x 4000 x 425) and configs[1] (598 x 2000 x 72), 30
+    iterations, in the launch configuration bench.py --config times (the whole cube in one
+    smf_retrieve); sampled columns, including plume columns, recomputed by the oracle one by
+    one. Pixels beyond tolerance go through the C18 ulp classifier (fail on any
+    well-conditioned one)."""
+    from parity_util import c18_classify
+    cfg = synth.CONFIGS[name]
+    cube, s, _ = synth.generate(cfg)
     enh, alb, st, mu, q, _ = run_gpu(smf, torch, cube, s, n_iter=cfg.n_iter)
-    a_ref, r_ref, st_ref = oracle.retrieve(cube, s, n_iter=cfg.n_iter)
-    assert (st == 0).all() and (st_ref == 0).all()
-    rep = assert_parity(enh, alb, a_ref, r_ref, "stress")
-    print(rep)
-    assert rep["zero_set_agreement"] > 0.999
+    assert (st == 0).all()
+    assert (enh >= 0).all() and np.isfinite(enh).all()
+    cols = _plume_columns(cfg, k=4, extra=3, seed=2)
+    for c in cols:
+        a_ref, r_ref, rc, dg = oracle.retrieve_column(cube[c], s, n_iter=cfg.n_iter, diagnostics=True)
+        assert rc == 0
+        rep = compare(enh[c], alb[c], a_ref, r_ref, f"{name} col {c}")
+        rep["q_rel"] = float(q[c] / dg["q"][-1] - 1)
+        print(rep)
+        assert rep["albedo_max_rel"] <= 1e-5
+        assert rep["n_nan_mismatch"] == 0 and rep["zero_set_agreement"] > 0.999, rep
+        if rep["n_bad"]:
+            cls = c18_classify(enh[c], a_ref, cube[c], s,
+                               lambda L, ss: oracle.retrieve_column(L, ss, n_iter=cfg.n_iter)[0], rep["tol"])
+            print("C18", c, cls)
+            assert not cls["well_conditioned"], cls
 
 
 # ------------------------------------------------------------------ energy trace (Eq. 8, NEXT f2)
@@ -283,6 +300,17 @@ def test_layout_conversion(smf, torch, layout):
     """On-disk BIL / BIP cubes -> [samples][lines][bands] on the device: exact copy."""
     rng = np.random.default_rng(5)
     lines, samples, bands = 37, 70, 45
+    cpb = rng.standard_normal((samples, lines, bands)).astype(np.float32)
+    disk = cpb.transpose(1, 2, 0) if layout == "BIL" else cpb.transpose(1, 0, 2)
+    out = smf.convert_layout(torch.from_numpy(np.ascontiguousarray(disk)).cuda(), layout).cpu().numpy()
+    np.testing.assert_array_equal(out, cpb)
+
+
+@pytest.mark.parametrize("layout", ["BIL", "BIP"])
+def test_layout_conversion_many_lines(smf, torch, layout):
+    """More lines than the 65535 grid-dimension limit: the kernels grid-stride."""
+    rng = np.random.default_rng(6)
+    lines, samples, bands = 70001, 3, 5
     cpb = rng.standard_normal((samples, lines, bands)).astype(np.float32)
     disk = cpb.transpose(1, 2, 0) if layout == "BIL" else cpb.transpose(1, 0, 2)
     out = smf.convert_layout(torch.from_numpy(np.ascontiguousarray(disk)).cuda(), layout).cpu().numpy()
@@ -592,3 +620,67 @@ def test_grouped_unaligned_remainder_wide(smf, torch):
         print(assert_parity(enh[c0:c1].reshape(-1), alb[c0:c1].reshape(-1), a_ref, r_ref, f"unaligned {c0}:{c1}"))
         assert abs(q[k].item() / d["q"][-1] - 1) < 1e-4
         np.testing.assert_allclose(mu[k].cpu().numpy(), d["mu"][-1], rtol=1e-6, atol=1e-9)
+
+
+def test_column_offset_views_match_separate_retrievals(smf, torch):
+    """Column sharding by pointer offset (what bench.py --split
+    columns and a multi-GPU caller do): smf_retrieve on two column-offset views of one
+    allocation equals two retrievals of separately allocated copies bit for bit, and the
+    whole-cube retrieval within C18 (the per-column reduction order depends on the grid)."""
+    for bands in (72, 13):
+        cfg = synth.scaled(synth.CONFIGS["segment"], cols=10, pixels=1500, bands=bands, rank=8)
+        cube, s, _ = synth.generate(cfg)
+        rad = torch.from_numpy(cube).cuda()
+        r = smf.Retriever(bands, s, n_iter=10)
+        views, copies = [], []
+        for c0, c1 in ((0, 6), (6, 10)):
+            for src, out in ((rad[c0:c1], views), (rad[c0:c1].clone(), copies)):
+                enh, alb, st = r.retrieve(src)
+                assert r.synchronize(st) == -1
+                out.append((enh.cpu().numpy(), alb.cpu().numpy()))
+        for (ev, av), (ec, ac) in zip(views, copies):
+            np.testing.assert_array_equal(ev, ec)
+            np.testing.assert_array_equal(av, ac)
+        enh, alb, st = r.retrieve(rad)
+        assert r.synchronize(st) == -1
+        ev = np.concatenate([v[0] for v in views])
+        av = np.concatenate([v[1] for v in views])
+        print(assert_parity(ev, av, enh.cpu().numpy().astype(np.float64), alb.cpu().numpy().astype(np.float64),
+                            f"views vs whole B={bands}"))
+
+
+@pytest.mark.xfail(strict=True, reason="recorded limitation (DESIGN.md 5.6): at N/B ~ 1.4 the fp32 sweep cannot "
+                   "reach the C18 bar on 1-2 well-conditioned pixels; the paper's regime is N >> B")
+def test_b626_short_column_c18_classification(smf, torch):
+    """B = 626 at N = 900 (N / B ~ 1.4, far outside the paper's N >> B regime, with no ridge):
+    the pixels beyond the C18 bar are classified by the ulp protocol and reported; the test
+    fails only on a well-conditioned mismatch (DESIGN.md 5.6 records the outcome)."""
+    from parity_util import c18_classify
+    cfg = synth.scaled(synth.CONFIGS["tiny"], cols=1, pixels=900, bands=626, rank=8)
+    cube, s, _ = synth.generate(cfg)
+    enh, alb, st, *_ = run_gpu(smf, torch, cube, s, n_iter=6)
+    a_ref, r_ref, rc = oracle.retrieve_column(cube[0], s, n_iter=6)
+    assert st[0] == rc
+    rep = compare(enh[0], alb[0], a_ref, r_ref, "B626 N900")
+    print(rep)
+    if rep["n_bad"]:
+        cls = c18_classify(enh[0], a_ref, cube[0], s, lambda L, ss: oracle.retrieve_column(L, ss, n_iter=6)[0],
+                           rep["tol"])
+        print("C18 B=626 N=900:", {k: v for k, v in cls.items() if k != "gpu" and k != "oracle"})
+        assert not cls["well_conditioned"], cls
+
+
+def test_nvtx_and_diagnostics_do_not_change_results(smf, torch):
+    """NVTX ranges and the per-iteration diagnostics kernel are observers: bitwise the same maps."""
+    cfg = synth.scaled(synth.CONFIGS["tiny"], cols=6)
+    cube, s, _ = synth.generate(cfg)
+    rad = torch.from_numpy(cube).cuda()
+    outs = []
+    for kw in (dict(), dict(nvtx=True), dict(diagnostics=True)):
+        r = smf.Retriever(cfg.bands, s, n_iter=cfg.n_iter, **kw)
+        enh, alb, st = r.retrieve(rad)
+        assert r.synchronize(st) == -1
+        outs.append((enh.cpu().numpy(), alb.cpu().numpy()))
+    for e, a in outs[1:]:
+        np.testing.assert_array_equal(e, outs[0][0])
+        np.testing.assert_array_equal(a, outs[0][1])
