@@ -174,13 +174,15 @@ smf_status smf_initial_statistics(smf_ctx* ctx, const float* radiance, int cols,
                                   void* stream);
 
 /* Which kernel computes the initial statistics (Fig. alg lines 2-3, the
- * batched bands x bands SYRK): SMF_STATS_AUTO (default: tensor cores where the
- * shape fits, FFMA register tiles otherwise), SMF_STATS_FFMA (fp32 FFMA 8x8
- * register tiles), SMF_STATS_TENSOR (tcgen05 kind::tf32 with the two-term
- * accuracy-preserving split of DESIGN.md 5.5; SMF_ERR_SHAPE if this band count
- * has no tensor-core variant). smf_stats_kernel_used returns the kernel AUTO
- * resolves to (SMF_STATS_FFMA or SMF_STATS_TENSOR), -1 for a NULL context. */
-enum { SMF_STATS_AUTO = 0, SMF_STATS_FFMA = 1, SMF_STATS_TENSOR = 2 };
+ * batched bands x bands SYRK): SMF_STATS_AUTO (default: the narrow path's tf32
+ * tensor-core kernel where the shape fits, the wide path's int8 kernel), SMF_STATS_FFMA
+ * (fp32 FFMA 8x8 register tiles), SMF_STATS_TENSOR (tcgen05 kind::tf32 with the
+ * two-term accuracy-preserving split of DESIGN.md 5.5; SMF_ERR_SHAPE if this band
+ * count has no tensor-core variant), SMF_STATS_INT8 (wide path only, DESIGN.md 5.6:
+ * tcgen05 kind::i8 on a three-digit fixed-point split with exact int32 accumulation;
+ * SMF_ERR_SHAPE for narrow band counts). smf_stats_kernel_used returns the kernel AUTO
+ * resolves to, -1 for a NULL context. */
+enum { SMF_STATS_AUTO = 0, SMF_STATS_FFMA = 1, SMF_STATS_TENSOR = 2, SMF_STATS_INT8 = 3 };
 smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind);
 int smf_stats_kernel_used(const smf_ctx* ctx);
 

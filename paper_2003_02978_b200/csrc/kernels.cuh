@@ -781,10 +781,14 @@ struct PilotArgs {
     int cols, N, B;
     int mask;
     float nodata;
+    unsigned* vmax;   // wide int8 statistics: per-row maxima [cols][BEq], zeroed here (or NULL)
+    int BEq;
 };
 
 __global__ void k0_pilot(PilotArgs a) {
     const int c = blockIdx.x, tid = threadIdx.x;
+    if (a.vmax)
+        for (int b = tid; b < a.BEq; b += blockDim.x) a.vmax[(size_t)c * a.BEq + b] = 0u;
     __shared__ double cc;
     __shared__ double scratch[32];
     const int np = min(kPilotRows, a.N);

@@ -22,6 +22,7 @@
 #include "../../include/smf.h"
 #include "kernels.cuh"
 #include "wide.cuh"
+#include "widei8.cuh"
 
 using namespace smf;
 
@@ -163,7 +164,9 @@ struct Plan {
     int G1, S1, W1, T1, tpc1, NT1, be_full;
     bool k1tc;
     // wide path (any B): K1w block grid, K3w tiles of kWideT3 pixels
-    bool wide, widetc;
+    bool wide, widetc, widei8;
+    int R8, Np8, BEq8;          // int8 statistics: extended rows B + 2, padded pixels, vmax stride
+    size_t o_vmax, o_slices;
     int BEw, NBw, NGw, NBLKw;
     size_t o_sigma;
     long long ttot1;
@@ -218,7 +221,10 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.NBw = (p.BEw / 8) * (p.BEw / 8 + 1) / 2;
     p.NGw = (p.NBw + kWideNT1 - 1) / kWideNT1;
     p.NBLKw = (B + 2 + 127) / 128;
-    p.widetc = p.wide && ctx->stats_kernel != SMF_STATS_FFMA;
+    p.widetc = p.wide && ctx->stats_kernel == SMF_STATS_TENSOR;
+    p.widei8 = p.wide && (ctx->stats_kernel == SMF_STATS_AUTO || ctx->stats_kernel == SMF_STATS_INT8);
+    p.R8 = B + 2;
+    p.Np8 = (N + 15) / 16 * 16;
     p.k1tc = !p.wide && ctx->stats_kernel != SMF_STATS_FFMA && k1tc_fits(B);
     p.T1 = p.k1tc ? kTileTC : k1_rows(B);
     p.NT1 = p.k1tc ? K1TC<1>::NT : stats_threads(B);
@@ -233,7 +239,7 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     }
     p.W1 = p.k1tc ? p.be_full * p.be_full : k1_width_host(B);
     if (p.wide) {
-        p.smem1 = p.widetc ? k1w_tc_smem() : k1w_smem(B, p.BEw);
+        p.smem1 = p.widetc ? k1w_tc_smem() : (p.widei8 ? k1w_i8_smem() : k1w_smem(B, p.BEw));
         p.smem2 = k2w_init_smem(B);
         p.smem3 = k3w_smem(B);
     } else {
@@ -263,9 +269,13 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.o_pilot = take(cb * 4);
     p.o_ghat = take(cb * 4);
     const size_t bep = (size_t)p.NBLKw * 128;
-    p.o_part1 = p.wide ? take(p.widetc ? (size_t)cols * bep * bep * 8 : (size_t)cols * p.NGw * kWideNT1 * 64 * 8)
+    p.BEq8 = (int)bep;
+    p.o_part1 = p.wide ? take((p.widetc || p.widei8) ? (size_t)cols * bep * bep * 8
+                                                     : (size_t)cols * p.NGw * kWideNT1 * 64 * 8)
                        : take((size_t)p.G1 * p.S1 * p.W1 * 8);
-    p.o_sigma = take(p.widetc ? (size_t)cols * N * 4 : 0);
+    p.o_sigma = take((p.widetc || p.widei8) ? (size_t)cols * N * 4 : 0);
+    p.o_vmax = take(p.widei8 ? (size_t)cols * p.BEq8 * 4 : 0);
+    p.o_slices = take(p.widei8 ? (size_t)cols * kI8S * p.R8 * p.Np8 : 0);
     p.o_part3 = take((size_t)p.G * p.S * (B + kPartExtra) * 8);
     p.o_tra = take((size_t)cols * 8);
     p.o_rho = take((size_t)cols * 8);
@@ -277,7 +287,8 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     // wide literal covariance check (reading C16''): per-column fp64 scratch, aliased onto the
     // K1w partials (dead once k2w_init has consumed them) when they are large enough
     p.lit_stride = p.wide ? lit_doubles(B) : 0;
-    const size_t part1_bytes = p.wide ? (p.widetc ? (size_t)cols * bep * bep * 8 : (size_t)cols * p.NGw * kWideNT1 * 64 * 8)
+    const size_t part1_bytes = p.wide ? ((p.widetc || p.widei8) ? (size_t)cols * bep * bep * 8
+                                                                : (size_t)cols * p.NGw * kWideNT1 * 64 * 8)
                                       : 0;
     const size_t lit_bytes = (size_t)cols * p.lit_stride * 8;
     p.o_lit = !p.wide ? 0 : (lit_bytes <= part1_bytes ? p.o_part1 : take(lit_bytes));
@@ -657,6 +668,8 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     pa.B = p.B;
     pa.mask = ctx->mask;
     pa.nodata = ctx->nodata;
+    pa.vmax = p.widei8 ? (unsigned*)(ws + p.o_vmax) : nullptr;
+    pa.BEq = p.BEq8;
     {
         ProfScope ps(ctx, st, SMF_KERNEL_STATS);
         k0_pilot<<<p.cols, 128, 0, st>>>(pa);
@@ -664,6 +677,94 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k0_pilot launch");
     ++launches;
+    if (p.wide && p.widei8) {
+        // exact-integer tensor-core statistics (widei8.cuh): scan (sigma, row maxima) ->
+        // quantise to the int8 slice cube -> kind::i8 SYRK into the [BEp][BEp] partials
+        I8ScanArgs sc;
+        sc.L = rad;
+        sc.pil32 = pa.pil32;
+        sc.ghat32 = pa.ghat32;
+        sc.sigma = (float*)(ws + p.o_sigma);
+        sc.vmax = (unsigned*)(ws + p.o_vmax);
+        sc.cols = p.cols;
+        sc.N = p.N;
+        sc.B = p.B;
+        sc.BEq = p.BEq8;
+        sc.mask = ctx->mask;
+        sc.nodata = ctx->nodata;
+        {
+            ProfScope ps(ctx, st, SMF_KERNEL_STATS);
+            const dim3 grid((p.N + kI8ScanPix - 1) / kI8ScanPix, p.cols);
+            switch (k1w_scan_j(p.B)) {
+                case 2: k1w_scan<2><<<grid, 256, 0, st>>>(sc); break;
+                case 4: k1w_scan<4><<<grid, 256, 0, st>>>(sc); break;
+                case 8: k1w_scan<8><<<grid, 256, 0, st>>>(sc); break;
+                case 14: k1w_scan<14><<<grid, 256, 0, st>>>(sc); break;
+                default: k1w_scan<20><<<grid, 256, 0, st>>>(sc); break;
+            }
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_scan launch");
+        ++launches;
+        I8QuantArgs qa;
+        qa.L = rad;
+        qa.pil32 = pa.pil32;
+        qa.sigma = sc.sigma;
+        qa.vmax = sc.vmax;
+        qa.slices = (int8_t*)(ws + p.o_slices);
+        qa.cols = p.cols;
+        qa.N = p.N;
+        qa.B = p.B;
+        qa.R = p.R8;
+        qa.Np = p.Np8;
+        qa.BEq = p.BEq8;
+        qa.mask = ctx->mask;
+        e = cudaFuncSetAttribute(k1w_quant, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1w_quant_smem());
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_quant smem attribute");
+        {
+            ProfScope ps(ctx, st, SMF_KERNEL_STATS);
+            k1w_quant<<<dim3((p.Np8 + kI8QTile - 1) / kI8QTile, (p.R8 + kI8QRows - 1) / kI8QRows, p.cols), 256,
+                        k1w_quant_smem(), st>>>(qa);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_quant launch");
+        ++launches;
+        CUtensorMap tq;
+        {
+            cuuint64_t dims[3] = {(cuuint64_t)p.Np8, (cuuint64_t)p.R8, (cuuint64_t)p.cols * kI8S};
+            cuuint64_t strides[2] = {(cuuint64_t)p.Np8, (cuuint64_t)p.R8 * p.Np8};
+            cuuint32_t box[3] = {(cuuint32_t)kI8Tile, (cuuint32_t)kI8Blk, 1};
+            cuuint32_t estr[3] = {1, 1, 1};
+            memset(&tq, 0, sizeof(tq));
+            CUresult cr = g_encode(&tq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)qa.slices, dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (cr != CUDA_SUCCESS) {
+                set_err(ctx, "cuTensorMapEncodeTiled (int8 slices) failed (%d)", (int)cr);
+                return SMF_ERR_CUDA;
+            }
+        }
+        I8SyrkArgs ya;
+        ya.vmax = sc.vmax;
+        ya.part = (double*)(ws + p.o_part1);
+        ya.cols = p.cols;
+        ya.N = p.N;
+        ya.R = p.R8;
+        ya.BEq = p.BEq8;
+        ya.BEp = p.NBLKw * 128;
+        ya.NBLK = p.NBLKw;
+        ya.npairs = p.NBLKw * (p.NBLKw + 1) / 2;
+        ya.nitems = p.cols * ya.npairs;
+        e = cudaFuncSetAttribute(k1w_syrk_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1w_i8_smem());
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_syrk_i8 smem attribute");
+        {
+            ProfScope ps(ctx, st, SMF_KERNEL_STATS);
+            k1w_syrk_i8<<<std::min(ya.nitems, ctx->sm_count), kI8NT, k1w_i8_smem(), st>>>(tq, ya);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_syrk_i8 launch");
+        ++launches;
+    }
     if (p.wide && p.widetc) {
         float* sigma = (float*)(ws + p.o_sigma);
         {
@@ -710,7 +811,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         wa.NG = p.NGw;
         wa.mask = ctx->mask;
         wa.nodata = ctx->nodata;
-        if (!p.widetc) {
+        if (!p.widetc && !p.widei8) {
             e = cudaFuncSetAttribute(k1w_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem1);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_stats smem attribute");
             {
@@ -725,7 +826,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         ia.cs = col_state(p, ws, ctx->s_dev, ctx);
         ia.pil32 = pa.pil32;
         ia.part = wa.part;
-        ia.BEp = p.widetc ? p.NBLKw * 128 : 0;
+        ia.BEp = (p.widetc || p.widei8) ? p.NBLKw * 128 : 0;
         ia.mean_out = mean_out;
         ia.cov_out = cov_out;
         ia.cols = p.cols;
@@ -1047,7 +1148,11 @@ smf_status smf_iteration_diagnostics(smf_ctx* ctx, const void* workspace, int co
 }
 
 smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind) {
-    if (!ctx || kind < SMF_STATS_AUTO || kind > SMF_STATS_TENSOR) return SMF_ERR_INVALID_ARGUMENT;
+    if (!ctx || kind < SMF_STATS_AUTO || kind > SMF_STATS_INT8) return SMF_ERR_INVALID_ARGUMENT;
+    if (kind == SMF_STATS_INT8 && narrow(ctx->bands)) {
+        set_err(ctx, "int8 statistics kernel is the wide path's (bands %d use the narrow kernels)", ctx->bands);
+        return SMF_ERR_SHAPE;
+    }
     ++ctx->gen;
     if (kind == SMF_STATS_TENSOR && narrow(ctx->bands) && !k1tc_fits(ctx->bands)) {
         set_err(ctx, "tensor-core statistics kernel unavailable for %d bands", ctx->bands);
@@ -1060,6 +1165,8 @@ smf_status smf_set_stats_kernel(smf_ctx* ctx, int kind) {
 int smf_stats_kernel_used(const smf_ctx* ctx) {
     if (!ctx) return -1;
     const bool tc = narrow(ctx->bands) ? k1tc_fits(ctx->bands) : true;
+    if (!narrow(ctx->bands) && (ctx->stats_kernel == SMF_STATS_AUTO || ctx->stats_kernel == SMF_STATS_INT8))
+        return SMF_STATS_INT8;
     return (ctx->stats_kernel != SMF_STATS_FFMA && tc) ? SMF_STATS_TENSOR : SMF_STATS_FFMA;
 }
 

@@ -129,7 +129,7 @@ def _record(tensors, stream, device):
 class Retriever:
     """A library context (smf_ctx) bound to the current CUDA device."""
 
-    STATS_KERNELS = {"auto": 0, "ffma": 1, "tensor": 2}
+    STATS_KERNELS = {"auto": 0, "ffma": 1, "tensor": 2, "int8": 3}
     COV_CHECKS = {"off": 0, "auto": 1, "always": 2}
 
     def __init__(self, bands, s, n_iter=30, use_sparsity=True, use_albedo=True, eps=1e-2, ridge_rel=0.0,
@@ -191,8 +191,9 @@ class Retriever:
 
     @property
     def stats_kernel_used(self) -> str:
-        """'tensor' (tcgen05 kind::tf32, split) or 'ffma': the kernel computing mu0, C0."""
-        return {1: "ffma", 2: "tensor"}[_lib.smf_stats_kernel_used(self._h)]
+        """'tensor' (tcgen05 kind::tf32, split), 'int8' (tcgen05 kind::i8, wide path) or 'ffma':
+        the kernel computing mu0, C0."""
+        return {1: "ffma", 2: "tensor", 3: "int8"}[_lib.smf_stats_kernel_used(self._h)]
 
     def _check(self, rc, h="self"):
         if rc != SMF_OK:

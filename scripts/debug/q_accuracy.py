@@ -11,7 +11,7 @@ for bands in (12, 13, 16, 32, 33):
     cfg = synth.scaled(synth.CONFIGS["tiny"], cols=4, pixels=500, bands=bands, rank=8)
     cube, s, _ = synth.generate(cfg)
     refs = [oracle.retrieve_column(cube[c], s, n_iter=12, diagnostics=True)[3]["q"] for c in range(4)]
-    for kw in (dict(), dict(stats_kernel="ffma"), dict(cov_check="always")):
+    for kw in (dict(), dict(stats_kernel="ffma"), dict(cov_check="always")) + ((dict(stats_kernel="tensor"),) if bands % 4 else ()):
         r = smf.Retriever(bands, s, n_iter=12, diagnostics=True, **kw)
         rad = torch.from_numpy(cube).cuda()
         ws = r.alloc_workspace(4, 500)

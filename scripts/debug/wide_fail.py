@@ -22,7 +22,7 @@ for name, sc, n_iter, cols in cases:
         cols = cols or sorted(set(list(hot[::max(1, len(hot) // 6)][:6]) + [0, 300]))
         cube, s, _ = synth.generate(cfg, columns=cols)
     refs = [oracle.retrieve_column(cube[c], s, n_iter=n_iter) for c in range(cube.shape[0])]
-    for kern in ("tensor", "ffma"):
+    for kern in ("int8", "tensor", "ffma"):
         r = smf.Retriever(cube.shape[2], s, n_iter=n_iter, stats_kernel=kern)
         enh, alb, st = r.retrieve(torch.from_numpy(cube).cuda())
         r.synchronize(st)
