@@ -1273,12 +1273,14 @@ __device__ int literal_iteration(const UpdateArgs& a, int c, const double* A0inv
         t[b] = mu[b] * (double)cs.s[b];
     }
     __syncthreads();
-    // A0^-1 t^k for the next iteration's Woodbury (y' of U = [t', t, h])
-    for (int b = tid; b < B; b += nt) {
-        double y = 0.0;
-        for (int i = 0; i < B; ++i) y = fma(A0inv[(size_t)i * B + b], t[i], y);
-        cs.yprev[(size_t)c * B + b] = y;
-    }
+    // A0^-1 t^k for the next iteration's Woodbury (y' of U = [t', t, h]); the wide path
+    // (A0inv = NULL) keeps L^-1 t^k instead and computes it after this call
+    if (A0inv)
+        for (int b = tid; b < B; b += nt) {
+            double y = 0.0;
+            for (int i = 0; i < B; ++i) y = fma(A0inv[(size_t)i * B + b], t[i], y);
+            cs.yprev[(size_t)c * B + b] = y;
+        }
     __syncthreads();
     // lines 12-14: C^k = (1/N) sum d_i d_i^T, P residual rows at a time
     const int E = B * (B + 1) / 2;

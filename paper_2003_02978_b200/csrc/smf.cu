@@ -535,8 +535,8 @@ int wide_blocks_per_sm(int B) {
 // tile (two buffers of kWideT3 rows) fits in shared memory
 bool supported(int B) {
     if (narrow(B)) return true;
-    return B >= 1 && k3w_j(B) > 0 && B <= kWideNT2 * kWideMaxBPT2 && k3w_smem(B) <= 220 * 1024 &&
-           k2w_init_smem(B) <= 200 * 1024 && k1w_smem(B, (B + 2 + 7) / 8 * 8) <= 220 * 1024;
+    return B >= 1 && k3w_j(B) > 0 && k3w_smem(B) <= 220 * 1024 &&
+           k2w_init_smem(B) <= 220 * 1024 && k1w_smem(B, (B + 2 + 7) / 8 * 8) <= 220 * 1024;
 }
 
 CUresult make_maps(const float* rad, int cols, int N, int B, CUtensorMap* main_map, CUtensorMap* tail_map,
@@ -836,6 +836,8 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         ia.NG = p.NGw;
         ia.use_albedo = ctx->use_albedo;
         ia.stats_only = stats_only;
+        ia.energy = ctx->energy;
+        ia.sym = p.widei8 ? 1 : 0;
         ia.ridge_rel = ctx->ridge;
         e = cudaFuncSetAttribute(k2w_init, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem2);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init smem attribute");
@@ -1330,7 +1332,7 @@ static smf_status retrieve_eager(smf_ctx* ctx, const float* radiance, int cols, 
     da.lit = (int*)(ws + p.o_dlit);
     da.cols = cols;
     da.N = pixels;
-    const size_t smem_up = p.wide ? k2w_update_smem(p.B) : (size_t)p.B * p.B * 8;
+    const size_t smem_up = p.wide ? k2w_update_smem(p.B, ctx->energy) : (size_t)p.B * p.B * 8;
     void* ufn = p.wide ? reinterpret_cast<void*>(&k2w_update) : reinterpret_cast<void*>(&k2_update);
     cudaError_t e0 = cudaFuncSetAttribute(ufn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_up);
     if (e0 != cudaSuccess) return cuda_fail(ctx, e0, "k2_update smem attribute");

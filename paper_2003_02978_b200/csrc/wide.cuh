@@ -10,16 +10,19 @@
 //                  through a shared-memory tile (the NG CTAs of a column are launch-
 //                  adjacent, so the column is read from HBM once and from L2 NG times).
 //  K2w k2w_init    lines 2-3, 5-6: C0 from the blocks (fp64), ridge, blocked in-place
-//                  Gauss-Jordan inverse A^-1 = (C0 + rho I)^-1 in global memory (the
+//                  Cholesky A0 = C0 + rho I = L L^T in global memory (wide_chol.cuh; the
 //                  B x B fp64 matrix, 1.44 MB at B = 425, exceeds shared memory),
-//                  z0 = A^-1 t0, q0, mhat.
-//      k2w_update  lines 9-16: the narrow Woodbury update with A^-1 streamed from
-//                  global memory.
+//                  z0 = L^-T L^-1 t0, q0, mhat.
+//      k2w_update  lines 9-16: the Woodbury update of the narrow path on the Cholesky
+//                  factor (forward solves for W = L^-1 U, one backward solve for z).
+//  The statistics themselves default to the exact-integer tensor-core kernels of
+//  widei8.cuh (k1w_stats / k1w_stats_tc remain selectable).
 //  K3w k3w_sweep   per pixel (albedo, projection, thresholded update, beta) with a
 //                  warp per pixel over a shared-memory tile of contiguous pixel rows,
 //                  then the sufficient statistics sum beta L' with a thread per band.
 #pragma once
 #include "kernels.cuh"
+#include "wide_chol.cuh"
 
 namespace smf {
 
@@ -207,10 +210,8 @@ __global__ void __launch_bounds__(kWideNT1, 2) k1w_stats(WideStatsArgs a) {
 }
 
 // ---------------------------------------------------------------- K2w init
-constexpr int kWideNT2 = 256;
-constexpr int kWideNTI = 512;     // k2w_init: a thread per matrix column (B <= 512) in the GJ updates
-constexpr int kWideMaxBPT2 = 4;   // bands per thread in k2w_update (B <= 1024)
-constexpr int kGJ = 32;          // Gauss-Jordan block size
+constexpr int kWideNT2 = 128;    // k2w_update threads (5 CTAs per SM: one wave of 598 columns)
+constexpr int kWideNTI = 256;     // k2w_init threads (1 CTA per SM: up to 255 registers for the register-resident diagonal factor)
 
 struct WideInitArgs {
     ColState cs;
@@ -220,116 +221,18 @@ struct WideInitArgs {
     double* mean_out;      // optional [cols][B]
     double* cov_out;       // optional [cols][B][B]
     int cols, N, B, BE, NG, use_albedo, stats_only;
+    int energy;            // the energy trace needs tr(A0^-1)
+    int sym;               // the block-pair partials are exactly symmetric (int8 SYRK): no (P + P^T)/2
     double ridge_rel;
 };
 
-__host__ inline size_t k2w_init_smem(int B) { return (size_t)(5 * B + kGJ * kGJ + (size_t)B * (kGJ + 2) + 32 * 4) * 8 + 16; }
-
-// In-place blocked Gauss-Jordan inverse of the SPD matrix A (B x B, row-major, global)
-// by one CTA: for every diagonal block K (kGJ wide), D = A_KK^-1 (shared memory,
-// unblocked GJ), R = D A_K* (row panel), A_ij -= A_iK R_Kj, A_iK = -A_iK D, A_KK = D.
-// The old column panel A_.K is staged in shared memory (Cp, row stride kGJ + 1) and
-// read as broadcasts by the thread-per-column trailing update; the new row panel stays
-// in registers. No pivoting: for an SPD matrix the pivots are the Cholesky pivots
-// squared; a pivot <= tol flags NOT_SPD.
-__device__ bool wide_gj_inverse(double* A, int B, double tol, double* D /* [kGJ][kGJ] */,
-                                double* Cp /* [B][kGJ + 2], 16-byte aligned */) {
-    constexpr int CS = kGJ + 2;   // even: rows 16-byte aligned for the double2 broadcasts
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int k0 = 0; k0 < B; k0 += kGJ) {
-        const int nb = min(kGJ, B - k0);
-        // stage D (zero-padded) and the column panel
-        for (int e = tid; e < kGJ * kGJ; e += nt) {
-            const int r = e / kGJ, cc = e % kGJ;
-            D[e] = (r < nb && cc < nb) ? A[(size_t)(k0 + r) * B + k0 + cc] : 0.0;
-        }
-        for (int e = tid; e < B * kGJ; e += nt) {
-            const int r = e / kGJ, cc = e % kGJ;
-            Cp[r * CS + cc] = cc < nb ? A[(size_t)r * B + k0 + cc] : 0.0;
-        }
-        __syncthreads();
-        // (a) D = inverse of the diagonal block (unblocked GJ)
-        for (int j = 0; j < nb; ++j) {
-            const double piv = D[j * kGJ + j];
-            if (!(piv > tol) || !isfinite(piv)) return false;   // uniform: D is shared
-            const double p = 1.0 / piv;
-            for (int e = tid; e < nb * nb; e += nt) {
-                const int r = e / nb, cc = e % nb;
-                if (r != j && cc != j) D[r * kGJ + cc] -= D[r * kGJ + j] * p * D[j * kGJ + cc];
-            }
-            __syncthreads();
-            for (int e = tid; e < nb; e += nt) {
-                if (e != j) {
-                    D[j * kGJ + e] *= p;
-                    D[e * kGJ + j] *= -p;
-                }
-            }
-            __syncthreads();
-            if (tid == 0) D[j * kGJ + j] = p;
-            __syncthreads();
-        }
-        // (b) row panel R_Kj = D A_Kj and (c) trailing update A_ij -= A_iK R_Kj, thread per
-        // column j outside the block
-        for (int j = tid; j < B; j += nt) {
-            if (j >= k0 && j < k0 + nb) continue;
-            double rn[kGJ];
-            {
-                double rp[kGJ];
-#pragma unroll
-                for (int s2 = 0; s2 < kGJ; ++s2) rp[s2] = s2 < nb ? A[(size_t)(k0 + s2) * B + j] : 0.0;
-#pragma unroll
-                for (int r = 0; r < kGJ; ++r) {
-                    double v = 0.0;
-#pragma unroll
-                    for (int s2 = 0; s2 < kGJ; ++s2) v = fma(D[r * kGJ + s2], rp[s2], v);
-                    rn[r] = v;
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < kGJ; ++r)
-                if (r < nb) A[(size_t)(k0 + r) * B + j] = rn[r];
-            // rows in groups of 8 so that 8 global loads are in flight per thread
-            for (int i0 = 0; i0 < B; i0 += 8) {
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int i = i0 + u;
-                    v[u] = (i < B && (i < k0 || i >= k0 + nb)) ? A[(size_t)i * B + j] : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int i = i0 + u;
-                    if (i >= B) break;
-                    if (i >= k0 && i < k0 + nb) continue;
-                    const double2* ci = reinterpret_cast<const double2*>(Cp + i * CS);
-                    double w0 = v[u], w1 = 0.0;
-#pragma unroll
-                    for (int s2 = 0; s2 < kGJ; s2 += 2) {
-                        const double2 cc = ci[s2 / 2];
-                        w0 = fma(-cc.x, rn[s2], w0);
-                        w1 = fma(-cc.y, rn[s2 + 1], w1);
-                    }
-                    A[(size_t)i * B + j] = w0 + w1;
-                }
-            }
-        }
-        // (d) column panel A_iK = -A_iK D (from the staged old panel), (e) A_KK = D
-        for (int i = tid; i < B; i += nt) {
-            if (i >= k0 && i < k0 + nb) continue;
-            const double* ci = Cp + i * CS;
-#pragma unroll 4
-            for (int r = 0; r < nb; ++r) {
-                double v = 0.0;
-#pragma unroll
-                for (int s2 = 0; s2 < kGJ; ++s2) v = fma(ci[s2], D[s2 * kGJ + r], v);
-                A[(size_t)i * B + k0 + r] = -v;
-            }
-        }
-        for (int e = tid; e < nb * nb; e += nt) A[(size_t)(k0 + e / nb) * B + k0 + e % nb] = D[(e / nb) * kGJ + e % nb];
-        __syncthreads();
-    }
-    return true;
+// shared: dm, srx, cv, vt, mh [B]; D, Dinv [32][33]; the panel Cp [B][34] (after the
+// factorisation reused for the solves: x [2][B], red [16][2][32], yv [2][32]); scratch [32][4]
+__host__ __device__ inline size_t k2w_init_panel(int B) {
+    const size_t p = (size_t)B * (kChB + 2), q = (size_t)2 * B + 16 * 2 * 32 + 2 * 32;
+    return p > q ? p : q;
 }
+__host__ inline size_t k2w_init_smem(int B) { return (size_t)(5 * B + 2 * kChB * kChD + k2w_init_panel(B) + 32 * 4) * 8 + 32; }
 
 __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     extern __shared__ double w2_smem[];
@@ -339,10 +242,11 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     double* cv = srx + B;        // [B] pilot c
     double* vt = cv + B;         // [B] t0
     double* mh = vt + B;         // [B] fp32 mhat (as double)
-    double* D = mh + B;          // [kGJ][kGJ]
-    double* Cp = D + kGJ * kGJ + ((5 * B) & 1);   // [B][kGJ + 2] column panel (16-byte aligned)
-    double* scratch = Cp + (size_t)B * (kGJ + 2);   // [32][4]
-    __shared__ int bad;
+    double* D = mh + B;          // [kChB][kChD] diagonal block
+    double* Dinv = D + kChB * kChD;                  // [kChB][kChD] its inverse
+    double* Cp = Dinv + kChB * kChD + ((5 * B) & 1);   // [B][kChB + 2] panel (16-byte aligned)
+    double* scratch = Cp + k2w_init_panel(B);   // [32][4]
+    __shared__ int bad, chol_flag;
     __shared__ double sh_tol, sh_mm;
     const int BEp = a.BEp;
     const double* S = BEp > 0 ? a.part + (size_t)c * BEp * BEp : a.part + (size_t)c * a.NG * kWideNT1 * 64;
@@ -355,7 +259,7 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
             i = k;
             k = t;
         }
-        if ((i >> 7) == (k >> 7)) return 0.5 * (S[(size_t)i * BEp + k] + S[(size_t)k * BEp + i]);
+        if (!a.sym && (i >> 7) == (k >> 7)) return 0.5 * (S[(size_t)i * BEp + k] + S[(size_t)k * BEp + i]);
         return S[(size_t)i * BEp + k];
     };
     double* A = a.cs.ainv + (size_t)c * B * B;
@@ -378,14 +282,17 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     }
     __syncthreads();
     // C0 = (Sxx + Srx c^T + c Srx^T + Srr c c^T)/N - dm dm^T  (fp64, lower + mirror)
-    for (size_t e = tid; e < (size_t)B * B; e += nt) {
-        const int i = (int)(e / B), k = (int)(e % B);
-        if (i < k) continue;
+    // a warp per row, lanes over the columns k <= i (coalesced partial reads, no divisions)
+    for (int i = tid >> 5; i < B; i += nt >> 5)
+        for (int k = tid & 31; k <= i; k += 32) {
         const double s2 = ext(i, k) + srx[i] * cv[k] + cv[i] * srx[k] + Srr * cv[i] * cv[k];
         const double v = s2 * invN - dm[i] * dm[k];
         if (!isfinite(v)) nonfinite = 1;
-        A[(size_t)i * B + k] = v;
-        A[(size_t)k * B + i] = v;
+        A[(size_t)i * B + k] = v;   // lower triangle only (the Cholesky reads nothing else)
+        if (a.cov_out) {
+            a.cov_out[(size_t)c * B * B + (size_t)i * B + k] = v;
+            a.cov_out[(size_t)c * B * B + (size_t)k * B + i] = v;
+        }
     }
     if (nonfinite && bad == COL_OK) atomicCAS(&bad, COL_OK, COL_NONFINITE);
     __syncthreads();
@@ -396,8 +303,6 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
         if (a.mean_out) a.mean_out[(size_t)c * B + b] = m;
         dm[b] = m;
     }
-    if (a.cov_out)
-        for (size_t e = tid; e < (size_t)B * B; e += nt) a.cov_out[(size_t)c * B * B + e] = A[e];
     if (a.stats_only) return;
     __syncthreads();
     {
@@ -424,7 +329,7 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
         __syncthreads();
     }
     int st = bad;
-    if (st == COL_OK && !wide_gj_inverse(A, B, sh_tol, D, Cp)) st = COL_NOT_SPD;
+    if (st == COL_OK && !wide_cholesky(A, B, sh_tol, D, Dinv, Cp, &chol_flag)) st = COL_NOT_SPD;
     __syncthreads();
     const double mm = sh_mm;
     for (int b = tid; b < B; b += nt) {
@@ -433,23 +338,26 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
         a.cs.mhat32[(size_t)c * B + b] = m32;
         mh[b] = (double)m32;
     }
+    // z0 = A0^-1 t0 = L^-T (L^-1 t0); L^-1 t0 is kept (yprev) for the first Woodbury update
+    double* xw = Cp;                    // [B]
+    double* xz = Cp + B;                // [B]
+    double* red = Cp + 2 * (size_t)B;   // [nwarps][2][32]
+    double* yv = red + 16 * 2 * 32;     // [2][32]
+    for (int b = tid; b < B; b += nt) xw[b] = st == COL_OK ? vt[b] : 0.0;
     __syncthreads();
+    if (st == COL_OK) {   // uniform
+        tri_fwd<1>(A, B, xw, D, red, yv);
+        for (int b = tid; b < B; b += nt) xz[b] = xw[b];
+        __syncthreads();
+        tri_bwd<1>(A, B, xz, D, red, yv);
+    }
     double qc[3] = {0.0, 0.0, 0.0};
     for (int b = tid; b < B; b += nt) {
-        double y = 0.0;
-        int i = 0;
-        for (; i + 8 <= B; i += 8) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = A[(size_t)(i + u) * B + b];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) y = fma(v[u], vt[i + u], y);
-        }
-        for (; i < B; ++i) y = fma(A[(size_t)i * B + b], vt[i], y);
+        const double y = st == COL_OK ? xz[b] : 0.0;
         const float z32 = (float)y;
         a.cs.z32[(size_t)c * B + b] = z32;
         a.cs.tprev[(size_t)c * B + b] = vt[b];
-        a.cs.yprev[(size_t)c * B + b] = y;
+        a.cs.yprev[(size_t)c * B + b] = st == COL_OK ? xw[b] : 0.0;
         qc[0] += vt[b] * y;
         qc[1] += mh[b] * (double)z32;
         qc[2] += dm[b] * (double)z32;
@@ -465,9 +373,20 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
         a.cs.status[c] = st;
         a.cs.nlit[c] = 0;
     }
-    // tr((C0 + rho I)^-1) for the energy trace (fixed order)
+    // tr((C0 + rho I)^-1) = ||L^-1||_F^2 for the energy trace: forward solves of the unit
+    // vectors, four at a time (only when the trace is on)
     double tl[1] = {0.0};
-    for (int b = tid; b < B; b += nt) tl[0] += A[(size_t)b * B + b];
+    if (a.energy && st == COL_OK) {
+        double* xu = Cp;   // [2][B]
+        for (int i0 = 0; i0 < B; i0 += 2) {
+            __syncthreads();
+            for (int e = tid; e < 2 * B; e += nt) xu[e] = (e % B == i0 + e / B) ? 1.0 : 0.0;
+            __syncthreads();
+            tri_fwd<2>(A, B, xu, D, red, yv);
+            for (int e = tid; e < 2 * B; e += nt)
+                if (i0 + e / B < B) tl[0] += xu[e] * xu[e];
+        }
+    }
     block_sum<1>(tl, scratch);
     if (tid == 0) {
         a.cs.tra[c] = tl[0];
@@ -476,22 +395,35 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
 }
 
 // ---------------------------------------------------------------- K2w update
-__host__ inline size_t k2w_update_smem(int B) { return (size_t)(2 * B + 32 * 18) * 8; }
+// shared: t [B], x_f [2][B] (forward: t, h -> L^-1 t, L^-1 h), x_b [1 or 4][B] (backward
+// right-hand sides; 4 with the energy trace), diagonal block [32][33], reduction
+// [nwarps][2][32], yv [2][32], scratch [32][18]
+__host__ inline size_t k2w_update_smem(int B, int energy) {
+    return (size_t)((energy ? 7 : 4) * B + kChB * kChD + 4 * 2 * 32 + 2 * 32 + 32 * 18) * 8;
+}
 constexpr int kLitRows = 32;   // residual rows per chunk of the wide literal check
 // doubles of global scratch per column for the wide literal check (packed C^k + residual rows)
 __host__ inline long long lit_doubles(int B) { return (long long)B * (B + 1) / 2 + (long long)kLitRows * B; }
 
-__global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
+// Woodbury update on the Cholesky factor A0 = L L^T (wide_chol.cuh):
+// W = L^-1 U with U = [t', t, h] (w' = L^-1 t' kept from the previous update in yprev), G =
+// U^T A0^-1 U = W^T W, coef = M (I + G M)^-1 W^T w_t, z = L^-T (w_t - W coef). The energy trace
+// also needs Y = A0^-1 U = L^-T W (three more backward right-hand sides, same pass over L).
+__global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a) {
     extern __shared__ double w3_smem[];
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x, nt = blockDim.x;
-    double* sh_t = w3_smem;        // [B]
-    double* sh_h = sh_t + B;       // [B]
-    double* scratch = sh_h + B;    // [32][18]
+    double* sh_t = w3_smem;          // [B] t^k
+    double* xf = sh_t + B;           // [2][B]
+    double* xb = xf + 2 * B;         // [4][B]
+    double* Dsm = xb + (a.energy_on ? 4 : 1) * B;   // [32][33]
+    double* red = Dsm + kChB * kChD; // [4][2][32]
+    double* yv = red + 4 * 2 * 32;   // [2][32]
+    double* scratch = yv + 2 * 32;   // [32][18]
     __shared__ double sh_coef[3], sh_s[3];
     __shared__ int sh_st, sh_lit;
     ColState& cs = a.cs;
     if (cs.status[c] != COL_OK) return;   // uniform per block
-    const double* Ainv = cs.ainv + (size_t)c * B * B;
+    const double* Lf = cs.ainv + (size_t)c * B * B;   // Cholesky factor (lower, row-major)
     // 1. sufficient statistics of the previous sweep (fixed CTA order)
     const long long c0 = (long long)c * a.tpc, c1 = c0 + a.tpc;
     int b0 = (int)((c0 * a.G) / a.ttot);
@@ -514,11 +446,7 @@ __global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
     }
     __syncthreads();
     const double bbar = sh_s[0] * invN, b2 = sh_s[1] * invN, bs = sh_s[2] * invN;
-    double yt_r[kWideMaxBPT2], yh_r[kWideMaxBPT2];
-#pragma unroll
-    for (int jj = 0; jj < kWideMaxBPT2; ++jj) {
-        const int j = tid + jj * nt;
-        if (j >= B) break;
+    for (int j = tid; j < B; j += nt) {
         double sv = 0.0;
         for (int b = b0; b < a.G && tile_begin(b, a.ttot, a.G) < c1; ++b) {
             const int slot = c - (int)(tile_begin(b, a.ttot, a.G) / a.tpc);
@@ -528,52 +456,29 @@ __global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
         const double mb = cs.mbar[o], tp = cs.tprev[o], mhj = (double)cs.mhat32[o];
         const double h = sv * invN + (bs * mhj - bbar * mb);   // (1/N) sum beta (L - mu0)
         const double mu = mb - bbar * tp;                       // Eq. 10 / line 10
-        sh_t[j] = mu * (double)cs.s[j];                         // Eq. 9
-        sh_h[j] = h;
+        const double t = mu * (double)cs.s[j];                  // Eq. 9
+        sh_t[j] = t;
+        xf[j] = t;
+        xf[B + j] = h;
         cs.mu[o] = mu;
     }
     __syncthreads();
-    // 2. y_t = A^-1 t, y_h = A^-1 h (A^-1 symmetric: column access, coalesced); 3. G
-    double gv[18];   // G = U^T Y (9) and YY = Y^T Y (9)
+    // 2. W = L^-1 [t, h]; 3. G = W^T W with W = [w', w_t, w_h] (U^T A0^-1 U)
+    tri_fwd<2>(Lf, B, xf, Dsm, red, yv);
+    double gv[18];   // G (9) and, with the energy trace, YY = Y^T Y (9, filled after the backward pass)
 #pragma unroll
     for (int i = 0; i < 18; ++i) gv[i] = 0.0;
-#pragma unroll
-    for (int jj = 0; jj < kWideMaxBPT2; ++jj) {
-        const int j = tid + jj * nt;
-        if (j >= B) break;
-        double yt = 0.0, yh = 0.0;
-        int i = 0;
-        for (; i + 16 <= B; i += 16) {   // 16 independent loads in flight
-            double v[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) v[u] = __ldg(Ainv + (size_t)(i + u) * B + j);
-#pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                yt = fma(v[u], sh_t[i + u], yt);
-                yh = fma(v[u], sh_h[i + u], yh);
-            }
-        }
-        for (; i < B; ++i) {
-            const double v = __ldg(Ainv + (size_t)i * B + j);
-            yt = fma(v, sh_t[i], yt);
-            yh = fma(v, sh_h[i], yh);
-        }
-        yt_r[jj] = yt;
-        yh_r[jj] = yh;
+    for (int j = tid; j < B; j += nt) {
         const size_t o = (size_t)c * B + j;
-        const double u[3] = {cs.tprev[o], sh_t[j], sh_h[j]}, y[3] = {cs.yprev[o], yt, yh};
+        const double w[3] = {cs.yprev[o], xf[j], xf[B + j]};
+        const double u[3] = {cs.tprev[o], sh_t[j], 0.0};
+        (void)u;
 #pragma unroll
         for (int r = 0; r < 3; ++r)
 #pragma unroll
-            for (int q2 = 0; q2 < 3; ++q2) {
-                gv[r * 3 + q2] += u[r] * y[q2];
-                gv[9 + r * 3 + q2] += y[r] * y[q2];
-            }
+            for (int q2 = 0; q2 < 3; ++q2) gv[r * 3 + q2] += w[r] * w[q2];
     }
-    if (a.energy_on)
-        block_sum<18>(gv, scratch);
-    else
-        block_sum<9>(*reinterpret_cast<double(*)[9]>(gv), scratch);
+    block_sum<9>(*reinterpret_cast<double(*)[9]>(gv), scratch);
     if (tid == 0) {
         // C^k = C0 + U M U^T, M in the basis (t', t, h)
         const double M[3][3] = {{bbar * bbar, -bbar * bbar, 0.0}, {-bbar * bbar, b2, -1.0}, {0.0, -1.0, 0.0}};
@@ -596,28 +501,65 @@ __global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
         }
         sh_st = st;
         sh_lit = a.lit_mode == 2 || (a.lit_mode == 1 && (!solved || !(min_eig3(K) > kLitTau)));
-        if (a.energy_on) cs.tq[c] = woodbury_trace(M, gv, gv + 9, B, cs.rho64[c], cs.tra[c], bbar);
     }
     __syncthreads();
     if (sh_lit) {
-        // lines 10-16 literally (reading C16''), C^k and the residual rows in global scratch
+        // lines 10-16 literally (reading C16''), C^k and the residual rows in global scratch;
+        // then w' = L^-1 t^k for the next Woodbury update
         double* Cp = a.lit + (size_t)c * a.lit_stride;
-        const int stl = literal_iteration(a, c, Ainv, Cp, Cp + (size_t)B * (B + 1) / 2, kLitRows, w3_smem, scratch);
+        const int stl = literal_iteration(a, c, nullptr, Cp, Cp + (size_t)B * (B + 1) / 2, kLitRows, xf, scratch);
+        if (stl != COL_NOT_SPD) {
+            for (int j = tid; j < B; j += nt) xf[j] = cs.tprev[(size_t)c * B + j];
+            __syncthreads();
+            tri_fwd<1>(Lf, B, xf, Dsm, red, yv);
+            for (int j = tid; j < B; j += nt) cs.yprev[(size_t)c * B + j] = xf[j];
+        }
         if (tid == 0) {
             cs.status[c] = stl;
             cs.nlit[c] += 1;
         }
         return;
     }
-    // 4. z = y_t - Y M (I + G M)^-1 U^T A^-1 t (Woodbury), q, mhat.z, mu.z
-    double qc[3] = {0.0, 0.0, 0.0};
+    // 4. z = L^-T (w_t - W coef) (Woodbury); with the energy trace also Y = L^-T W
+    const int nr = a.energy_on ? 4 : 1;
+    for (int j = tid; j < B; j += nt) {
+        const double wp = cs.yprev[(size_t)c * B + j], wt = xf[j], wh = xf[B + j];
+        xb[j] = wt - (wp * sh_coef[0] + wt * sh_coef[1] + wh * sh_coef[2]);
+        if (nr == 4) {
+            xb[B + j] = wp;
+            xb[2 * B + j] = wt;
+            xb[3 * B + j] = wh;
+        }
+    }
+    __syncthreads();
+    if (nr == 4) {
+        tri_bwd<2>(Lf, B, xb, Dsm, red, yv);
+        tri_bwd<2>(Lf, B, xb + 2 * B, Dsm, red, yv);
+    } else {
+        tri_bwd<1>(Lf, B, xb, Dsm, red, yv);
+    }
+    if (a.energy_on) {
+        double yy[9];
 #pragma unroll
-    for (int jj = 0; jj < kWideMaxBPT2; ++jj) {
-        const int j = tid + jj * nt;
-        if (j >= B) break;
+        for (int i = 0; i < 9; ++i) yy[i] = 0.0;
+        for (int j = tid; j < B; j += nt) {
+            const double y[3] = {xb[B + j], xb[2 * B + j], xb[3 * B + j]};
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int q2 = 0; q2 < 3; ++q2) yy[r * 3 + q2] += y[r] * y[q2];
+        }
+        block_sum<9>(yy, scratch);
+        if (tid == 0) {
+            const double M[3][3] = {{bbar * bbar, -bbar * bbar, 0.0}, {-bbar * bbar, b2, -1.0}, {0.0, -1.0, 0.0}};
+            cs.tq[c] = woodbury_trace(M, gv, yy, B, cs.rho64[c], cs.tra[c], bbar);
+        }
+    }
+    // 5. q, mhat.z, mu.z; state for the next iteration (w' = L^-1 t)
+    double qc[3] = {0.0, 0.0, 0.0};
+    for (int j = tid; j < B; j += nt) {
         const size_t o = (size_t)c * B + j;
-        const double yt = yt_r[jj], yh = yh_r[jj], yp = cs.yprev[o];
-        const double z = yt - (yp * sh_coef[0] + yt * sh_coef[1] + yh * sh_coef[2]);
+        const double z = xb[j];
         const float z32 = (float)z;
         const double t = sh_t[j];
         qc[0] += t * z;
@@ -625,7 +567,7 @@ __global__ void __launch_bounds__(kWideNT2, 2) k2w_update(UpdateArgs a) {
         qc[2] += cs.mu[o] * (double)z32;
         cs.z32[o] = z32;
         cs.tprev[o] = t;
-        cs.yprev[o] = yt;
+        cs.yprev[o] = xf[j];
     }
     block_sum<3>(qc, scratch);
     if (tid == 0) {

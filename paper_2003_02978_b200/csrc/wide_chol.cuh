@@ -1,0 +1,323 @@
+// wide_chol.cuh -- the wide path's factorisation (Fig. alg line 16's (C + rho I)^-1 products,
+// P:358-381) as a Cholesky factor A0 = C0 + rho I = L L^T instead of an explicit inverse:
+//
+//  wide_cholesky   in-place right-looking blocked Cholesky of one column's A0 (row-major B x B
+//                  in global memory, lower triangle) by one CTA: a warp factors each 32 x 32
+//                  diagonal block in shared memory (pivot test of reading C16': a pivot <= tol
+//                  is NOT_SPD, as the oracle's Cholesky), a thread per row solves the panel
+//                  L_iK = A_iK L_KK^-T with the inverted diagonal block, and 4 x 4 register
+//                  tiles of the lower trailing triangle take A_ij -= L_iK . L_jK (j <= i)
+//                  with the panel staged in shared memory.
+//                  B^3/6 FMA -- a sixth of the Gauss-Jordan inverse it replaces -- and the
+//                  shrinking trailing triangle is the only global traffic.
+//  tri_fwd<NR>     L x = b for NR right-hand sides: per 32-row block an off-diagonal GEMV
+//                  with every load of the block in flight at once (threads stride columns,
+//                  a transpose-reduction per 16 rows), then x_J = L_JJ^-1 y_J with the
+//                  inverted diagonal block stored in the factor (no sequential chain).
+//  tri_bwd<NR>     L^T x = b, the same on the mirrored upper triangle (L^T stored there, so
+//                  the backward GEMV also reads rows).
+// The Woodbury update needs A0^-1 only through G = U^T A0^-1 U = W^T W with
+// W = L^-1 U (forward solves) and z = L^-T (L^-1 t - W coef) (one backward solve), so the
+// per-iteration reads of L are the same bytes the explicit inverse cost.
+#pragma once
+#include <cstdint>
+
+namespace smf {
+
+constexpr int kChB = 32;         // block width of the factorisation and the solves
+constexpr int kChD = kChB + 1;   // padded row stride of the shared diagonal block
+
+// Factor and invert the diagonal block at k0 (nb <= 32 rows) by the calling warp: stage
+// the lower part of A into D, factor it in registers (lane l holds row l; column j of L is
+// read across lanes with shuffles), invert it into Dinv (lane c computes column c).
+// Returns false (warp-uniformly) on a pivot <= tol or non-finite.
+__device__ bool chol_diag_warp(const double* A, int B, int k0, int nb, double tol, double* D, double* Dinv) {
+    const int lane = threadIdx.x & 31;
+    double r[kChB];
+#pragma unroll
+    for (int m = 0; m < kChB; ++m) r[m] = (lane < nb && m <= lane) ? A[(size_t)(k0 + lane) * B + k0 + m] : 0.0;
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < kChB; ++j) {
+        if (j < nb) {
+            const double d = __shfl_sync(0xffffffffu, r[j], j);
+            if (!(d > tol) || !isfinite(d)) ok = false;   // warp-uniform
+            const double g = sqrt(fmax(d, 0.0));
+            const double ginv = 1.0 / g;
+            if (lane == j) r[j] = g;
+            else if (lane > j) r[j] *= ginv;   // L_lj
+            const double lj = r[j];
+#pragma unroll
+            for (int m = j + 1; m < kChB; ++m) {
+                const double lmj = __shfl_sync(0xffffffffu, r[j], m);   // L_mj
+                if (lane >= m) r[m] = fma(-lj, lmj, r[m]);
+            }
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < kChB; ++m) D[lane * kChD + m] = r[m];
+    __syncwarp();
+    if (ok) {
+        double x[kChB];
+#pragma unroll
+        for (int i = 0; i < kChB; ++i) {
+            double v = i == lane ? 1.0 : 0.0;
+#pragma unroll
+            for (int k = 0; k < i; ++k) v = fma(-D[i * kChD + k], x[k], v);
+            x[i] = i < nb ? v * (1.0 / D[i * kChD + i]) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < kChB; ++i) Dinv[i * kChD + lane] = x[i];
+    }
+    __syncwarp();
+    return ok;
+}
+
+// 4 x 4 register tile (I, J) of the trailing update A_ij -= Cp_i . Cp_j (j <= i) below row
+// and right of column t0 (tile rows t0 + 4I.., columns t0 + 4J..).
+__device__ __forceinline__ void chol_tile(double* A, int B, int t0, int I, int J, const double* Cp) {
+    constexpr int CS = kChB + 2;
+    const int i0 = t0 + 4 * I, j0 = t0 + 4 * J;
+    double acc[4][4];
+#pragma unroll
+    for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2) acc[a2][b2] = 0.0;
+    const double2* ri[4];
+    const double2* rj[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        ri[q] = reinterpret_cast<const double2*>(Cp + min(i0 + q, B - 1) * CS);
+        rj[q] = reinterpret_cast<const double2*>(Cp + min(j0 + q, B - 1) * CS);
+    }
+    double old[4][4];   // the 16 old values in flight while the products accumulate
+#pragma unroll
+    for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2) {
+            const int i = i0 + a2, j = j0 + b2;
+            old[a2][b2] = (i < B && j <= i) ? A[(size_t)i * B + j] : 0.0;
+        }
+#pragma unroll 4
+    for (int s2 = 0; s2 < kChB / 2; ++s2) {
+        double2 va[4], vb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            va[q] = ri[q][s2];
+            vb[q] = rj[q][s2];
+        }
+#pragma unroll
+        for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+            for (int b2 = 0; b2 < 4; ++b2)
+                acc[a2][b2] = fma(va[a2].y, vb[b2].y, fma(va[a2].x, vb[b2].x, acc[a2][b2]));
+    }
+#pragma unroll
+    for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2) {
+            const int i = i0 + a2, j = j0 + b2;
+            if (i < B && j <= i) A[(size_t)i * B + j] = old[a2][b2] - acc[a2][b2];
+        }
+}
+
+__device__ __forceinline__ void tri_decode(int e, int& I, int& J) {
+    I = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+    while ((I + 1) * (I + 2) / 2 <= e) ++I;
+    while (I * (I + 1) / 2 > e) --I;
+    J = e - I * (I + 1) / 2;
+}
+
+// In-place Cholesky of A (row-major B x B, global; the lower triangle holds A on entry).
+// On exit the matrix holds the solve-ready factor M:
+//   off-diagonal blocks, lower: L;  upper: L^T (mirrored, so both solves read rows);
+//   diagonal blocks: lower (incl. diagonal) L_KK^-1, strictly upper (L_KK^-1)^T.
+// Look-ahead: once the trailing update has finished the next block column, warp 0 factors
+// the next diagonal block while the other warps apply the rest of the trailing update.
+// D, Dinv: shared [kChB][kChD]; Cp: shared [B][kChB + 2] (16-byte aligned rows); flag:
+// shared int. Returns false (uniformly) on a non-positive or non-finite pivot (<= tol).
+__device__ bool wide_cholesky(double* A, int B, double tol, double* D, double* Dinv, double* Cp, int* flag) {
+    constexpr int CS = kChB + 2;
+    const int tid = threadIdx.x, nt = blockDim.x, wid = tid >> 5;
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    if (wid == 0 && !chol_diag_warp(A, B, 0, min(kChB, B), tol, D, Dinv) && (tid & 31) == 0) *flag = 1;
+    __syncthreads();
+    if (*flag) return false;
+    for (int k0 = 0; k0 < B; k0 += kChB) {
+        const int nb = min(kChB, B - k0);
+        // (a) the factored block (D, Dinv) is final: write L_KK^-1 and its transpose
+        for (int e = tid; e < nb * nb; e += nt) {
+            const int r = e / nb, cc = e - r * nb;
+            A[(size_t)(k0 + r) * B + k0 + cc] = cc <= r ? Dinv[r * kChD + cc] : Dinv[cc * kChD + r];
+        }
+        // (b) panel: x = a L_KK^-T for every row below the block (thread per row), staged in
+        // Cp, written to the lower part and mirrored (L^T) into the upper part
+        for (int i = k0 + nb + tid; i < B; i += nt) {
+            double a_[kChB];
+            double* Ai = A + (size_t)i * B + k0;
+#pragma unroll
+            for (int s = 0; s < kChB; ++s) a_[s] = s < nb ? Ai[s] : 0.0;
+#pragma unroll
+            for (int s = 0; s < kChB; ++s) {
+                double v = 0.0;
+                if (s < nb) {
+#pragma unroll
+                    for (int t = 0; t <= s; ++t) v = fma(a_[t], Dinv[s * kChD + t], v);
+                    Ai[s] = v;
+                    A[(size_t)(k0 + s) * B + i] = v;
+                }
+                Cp[i * CS + s] = v;   // zero past nb
+            }
+        }
+        __syncthreads();
+        const int t0 = k0 + nb;
+        if (t0 >= B) break;
+        const int T = B - t0, n4 = (T + 3) >> 2, nb2 = min(kChB, T), c4 = (nb2 + 3) >> 2;
+        // (c1) the trailing tiles of the next block column (tile columns J < c4, rows I >= J)
+        {
+            const int tri = c4 * (c4 + 1) / 2, n1 = tri + (n4 - c4) * c4;
+            for (int e = tid; e < n1; e += nt) {
+                int I, J;
+                if (e < tri) {
+                    tri_decode(e, I, J);
+                } else {
+                    I = c4 + (e - tri) / c4;
+                    J = (e - tri) % c4;
+                }
+                chol_tile(A, B, t0, I, J, Cp);
+            }
+        }
+        __syncthreads();
+        // (a') warp 0 factors the next diagonal block while (c2) the other warps update the
+        // rest of the trailing triangle (tile columns J >= c4)
+        if (wid == 0) {
+            if (!chol_diag_warp(A, B, t0, nb2, tol, D, Dinv) && (tid & 31) == 0) *flag = 1;
+        } else {
+            const int m = n4 - c4, n2 = m * (m + 1) / 2;
+            for (int e = tid - 32; e < n2; e += nt - 32) {
+                int I, J;
+                tri_decode(e, I, J);
+                chol_tile(A, B, t0, I + c4, J + c4, Cp);
+            }
+        }
+        __syncthreads();
+        if (*flag) return false;
+    }
+    return true;
+}
+
+// y_r = x_r - sum_{cc in [cs, ce)} M[J0 + r][cc] x[cc] for the nb <= 32 rows of block J0 and NR
+// right-hand sides (x: shared [NR][B]); result in yv (shared [NR][32]). Threads stride the
+// columns (coalesced row segments, up to 16 rows' loads in flight per thread); a transpose-
+// reduction per 16 rows leaves row r's warp partial in one lane; red: shared [nwarps][NR][32].
+template <int NR>
+__device__ __forceinline__ void row_gemv(const double* __restrict__ M, int B, int J0, int nb, int cs, int ce,
+                                         const double* x, double* red, double* yv) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x, nw = nt >> 5;
+#pragma unroll 1
+    for (int rh = 0; rh < 2; ++rh) {
+        double acc[16][NR];
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+#pragma unroll
+            for (int q = 0; q < NR; ++q) acc[r][q] = 0.0;
+        if (rh * 16 < nb) {
+            for (int cc = cs + tid; cc < ce; cc += nt) {
+                double lv[16];
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    const int rr = rh * 16 + r;
+                    lv[r] = rr < nb ? M[(size_t)(J0 + rr) * B + cc] : 0.0;
+                }
+                double xv[NR];
+#pragma unroll
+                for (int q = 0; q < NR; ++q) xv[q] = x[q * B + cc];
+#pragma unroll
+                for (int r = 0; r < 16; ++r)
+#pragma unroll
+                    for (int q = 0; q < NR; ++q) acc[r][q] = fma(lv[r], xv[q], acc[r][q]);
+            }
+        }
+        // transpose-reduce: after the halvings lane l holds row (l & 15)'s partial over the
+        // 16 lanes that share bit 4; the last xor adds the other half
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+#pragma unroll
+            for (int off = 8; off >= 1; off >>= 1) {
+#pragma unroll
+                for (int i = 0; i < off; ++i) {
+                    const bool up = lane & off;
+                    const double send = up ? acc[i][q] : acc[i + off][q];
+                    const double keep = up ? acc[i + off][q] : acc[i][q];
+                    acc[i][q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                }
+            }
+            acc[0][q] += __shfl_xor_sync(0xffffffffu, acc[0][q], 16);
+            if (lane < 16) red[(wid * NR + q) * 32 + rh * 16 + lane] = acc[0][q];
+        }
+    }
+    __syncthreads();
+    if (wid == 0 && lane < nb) {
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += red[(w * NR + q) * 32 + lane];
+            yv[q * 32 + lane] = x[q * B + J0 + lane] - s;
+        }
+    }
+}
+
+// Stage diagonal block [J0, J0 + nb) of M (lower: L_JJ^-1, upper: its transpose) into Dsm.
+__device__ __forceinline__ void stage_diag(const double* __restrict__ M, int B, int J0, int nb, double* Dsm) {
+    for (int e = threadIdx.x; e < kChB * kChB; e += blockDim.x) {
+        const int i = e >> 5, l = e & 31;
+        Dsm[i * kChD + l] = (i < nb && l < nb) ? M[(size_t)(J0 + i) * B + J0 + l] : 0.0;
+    }
+}
+
+// L x = b in place for NR (1 or 2) right-hand sides x[nr * B + i] (shared). Whole block;
+// Dsm [kChB][kChD], red [nwarps][NR][32], yv [NR][32] shared.
+template <int NR>
+__device__ void tri_fwd(const double* __restrict__ M, int B, double* x, double* Dsm, double* red, double* yv) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int J0 = 0; J0 < B; J0 += kChB) {
+        const int nb = min(kChB, B - J0);
+        stage_diag(M, B, J0, nb, Dsm);
+        row_gemv<NR>(M, B, J0, nb, 0, J0, x, red, yv);
+        __syncwarp();
+        if (wid == 0 && lane < nb) {   // x_J = L_JJ^-1 y_J (lower part of the staged block)
+#pragma unroll
+            for (int q = 0; q < NR; ++q) {
+                double v = 0.0;
+                for (int r = 0; r <= lane; ++r) v = fma(Dsm[lane * kChD + r], yv[q * 32 + r], v);
+                x[q * B + J0 + lane] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// L^T x = b in place (the mirrored upper part holds L^T). Same shared buffers as tri_fwd.
+template <int NR>
+__device__ void tri_bwd(const double* __restrict__ M, int B, double* x, double* Dsm, double* red, double* yv) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int nblk = (B + kChB - 1) / kChB;
+    for (int jb = nblk - 1; jb >= 0; --jb) {
+        const int J0 = jb * kChB, nb = min(kChB, B - J0);
+        stage_diag(M, B, J0, nb, Dsm);
+        row_gemv<NR>(M, B, J0, nb, J0 + nb, B, x, red, yv);
+        __syncwarp();
+        if (wid == 0 && lane < nb) {   // x_J = L_JJ^-T y_J (upper part incl. the diagonal)
+#pragma unroll
+            for (int q = 0; q < NR; ++q) {
+                double v = 0.0;
+                for (int r = lane; r < nb; ++r) v = fma(Dsm[lane * kChD + r], yv[q * 32 + r], v);
+                x[q * B + J0 + lane] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace smf
