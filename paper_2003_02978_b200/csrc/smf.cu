@@ -207,7 +207,12 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.wide = !narrow(B);
     p.tpc = (N + (p.wide ? kWideT3 : kTileRows) - 1) / (p.wide ? kWideT3 : kTileRows);
     p.ttot = (long long)cols * p.tpc;
-    const int per_sm = std::max(1, p.wide ? wide_blocks_per_sm(B) : sweep_blocks_per_sm(B));
+    int per_sm = std::max(1, p.wide ? wide_blocks_per_sm(B) : sweep_blocks_per_sm(B));
+    static const int per_sm_env = [] {   // SMF_SWEEP_CTAS_PER_SM: sweep occupancy override (A/B)
+        const char* e = std::getenv("SMF_SWEEP_CTAS_PER_SM");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (per_sm_env > 0) per_sm = std::min(per_sm, per_sm_env);
     long long G = (long long)ctx->sm_count * per_sm;
     if (G > p.ttot) G = p.ttot;
     p.G = (int)G;
