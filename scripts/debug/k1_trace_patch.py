@@ -1,9 +1,19 @@
 """Insert clock64 event stamps into k1_stats_tc (kernels.cuh) and a trace reader into smf.cu,
-in place (debug aid: build a variant with mkvariant.sh, then restore the sources).
+in place (debug aid).
 Events per tile i of CTA 0 (group leaders: lane 0 of warps 0 and 4):
 0 raw ready, 1 sigma dot done, 2 operand stage free, 3 stores issued, 4 published,
 5 MMA start, 6 MMA issued, 7 TMA issue."""
-p = "paper_2003_02978_b200/csrc/kernels.cuh"
+import os
+import sys
+
+# Patches a COPY of the sources: usage `python <this> DIR` with DIR a directory holding a copy
+# of paper_2003_02978_b200/ (e.g. made by `git archive HEAD paper_2003_02978_b200 include | tar
+# -x -C DIR`); build it with `mkvariant.sh NAME DIR`. Refuses to touch the repository itself.
+ROOT = os.path.abspath(sys.argv[1]) if len(sys.argv) > 1 else None
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if ROOT is None or ROOT == REPO:
+    raise SystemExit("usage: %s COPY_DIR (a copy of the sources, not the repository)" % sys.argv[0])
+p = os.path.join(ROOT, "paper_2003_02978_b200/csrc/kernels.cuh")
 s = open(p).read()
 s = s.replace("""constexpr int kFlushTC = SMF_K1TC_FLUSH;""", """constexpr int kFlushTC = SMF_K1TC_FLUSH;
 __device__ unsigned long long g_k1trace[10][4096];
@@ -50,7 +60,7 @@ for a, b in reps:
     assert a in s, a[:70]
     s = s.replace(a, b, 1)
 open(p, "w").write(s)
-p = "paper_2003_02978_b200/csrc/smf.cu"
+p = os.path.join(ROOT, "paper_2003_02978_b200/csrc/smf.cu")
 s = open(p).read()
 s += """
 extern "C" int smf_debug_k1_trace(unsigned long long* host, int n) {

@@ -1,6 +1,16 @@
 """Insert clock64 phase stamps into k2_update (kernels.cuh) and a reader into smf.cu, in place
-(debug aid: build a variant with mkvariant.sh, then restore the sources)."""
-p = "paper_2003_02978_b200/csrc/kernels.cuh"
+(debug aid)."""
+import os
+import sys
+
+# Patches a COPY of the sources: usage `python <this> DIR` with DIR a directory holding a copy
+# of paper_2003_02978_b200/ (e.g. made by `git archive HEAD paper_2003_02978_b200 include | tar
+# -x -C DIR`); build it with `mkvariant.sh NAME DIR`. Refuses to touch the repository itself.
+ROOT = os.path.abspath(sys.argv[1]) if len(sys.argv) > 1 else None
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if ROOT is None or ROOT == REPO:
+    raise SystemExit("usage: %s COPY_DIR (a copy of the sources, not the repository)" % sys.argv[0])
+p = os.path.join(ROOT, "paper_2003_02978_b200/csrc/kernels.cuh")
 s = open(p).read()
 s = s.replace("__global__ void __launch_bounds__(128, 5) k2_update(UpdateArgs a) {",
               "__device__ unsigned long long g_k2trace[64][8];\n"
@@ -27,7 +37,7 @@ for a, b in reps:
     assert a in s, a[:60]
     s = s.replace(a, b, 1)
 open(p, "w").write(s)
-p = "paper_2003_02978_b200/csrc/smf.cu"
+p = os.path.join(ROOT, "paper_2003_02978_b200/csrc/smf.cu")
 s = open(p).read()
 s += """
 extern "C" int smf_debug_k2_trace(unsigned long long* host, int n) {
