@@ -728,7 +728,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_quant smem attribute");
         {
             ProfScope ps(ctx, st, SMF_KERNEL_STATS);
-            k1w_quant<<<dim3((p.Np8 + kI8QTile - 1) / kI8QTile, (p.R8 + kI8QRows - 1) / kI8QRows, p.cols), 256,
+            k1w_quant<<<dim3((p.Np8 + kI8QTile * kI8QTiles - 1) / (kI8QTile * kI8QTiles), (p.R8 + kI8QRows - 1) / kI8QRows, p.cols), 256,
                         k1w_quant_smem(), st>>>(qa);
         }
         e = cudaGetLastError();

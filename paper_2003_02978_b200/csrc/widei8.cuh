@@ -145,8 +145,9 @@ struct I8QuantArgs {
 };
 
 constexpr int kI8QRows = 64;   // extended rows per k1w_quant block
+constexpr int kI8QTiles = 4;   // 128-pixel tiles per k1w_quant block (amortises the per-row setup)
 
-// grid (ceil(Np / 128), ceil(R / 64), cols), 256 threads, k1w_quant_smem() dynamic smem.
+// grid (ceil(Np / 512), ceil(R / 64), cols), 256 threads, k1w_quant_smem() dynamic smem.
 // Every extended row is v = fma(-sigma, beta_r, L_r) + gamma_r (band rows: beta = c_r, gamma =
 // 0, bit-identical to k1w_scan's v; rho row: beta = -1, gamma = -1; the 1 row: beta = 0,
 // gamma = 1; rows >= R: 0). A non-finite v becomes 0 -- which also zeroes nodata pixels
@@ -154,73 +155,78 @@ constexpr int kI8QRows = 64;   // extended rows per k1w_quant block
 // k1w_scan (+inf row maximum) and turns the partial into NaN in the SYRK epilogue.
 __global__ void __launch_bounds__(256) k1w_quant(I8QuantArgs a) {
     extern __shared__ uint32_t qsm[];   // [4][64 rows][33 words]: 4 pixels per word, padded
-    const int pt = blockIdx.x, rb = blockIdx.y, c = blockIdx.z, tid = threadIdx.x;
+    const int rb = blockIdx.y, c = blockIdx.z, tid = threadIdx.x;
     const int B = a.B, R = a.R;
     __shared__ float sh_sig[kI8QTile];
-    const int pbase = pt * kI8QTile, rbase = rb * kI8QRows;
-    for (int p = tid; p < kI8QTile; p += blockDim.x) {
-        const int gp = pbase + p;
-        sh_sig[p] = gp < a.N ? a.sigma[(size_t)c * a.N + gp] : __int_as_float(0x7fc00000);
-    }
-    // thread = (row r, pixel quads w = q + 4 u, u = 0..7: 32 pixels)
+    const int rbase = rb * kI8QRows;
+    // per-thread row constants, once per block (the block walks kI8QTiles pixel tiles)
     const int r = tid & (kI8QRows - 1), q = tid >> 6, gr = rbase + r;
     const unsigned vb = gr < R ? a.vmax[(size_t)c * a.BEq + gr] : 0u;
     const float sc = ldexpf(1.f, 27 - i8_exponent(vb));
     const float beta = gr < B ? a.pil32[(size_t)c * B + gr] : (gr == B ? -1.f : 0.f);
     const float gamma = gr == B ? -1.f : (gr == B + 1 ? 1.f : 0.f);
     const bool band = gr < B;
-    const int nvalid = a.N - pbase;   // pixels of this tile that exist (may exceed 128)
-    __syncthreads();
-    const float* Lr = a.L + ((size_t)c * a.N + pbase) * B + gr;
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-        float lv[4][4];   // 16 radiances in flight per thread
+    const int nrows = min(kI8QRows, R - rbase);
+    for (int pt = blockIdx.x * kI8QTiles; pt < min((int)(blockIdx.x + 1) * kI8QTiles, (a.Np + kI8QTile - 1) / kI8QTile);
+         ++pt) {
+        const int pbase = pt * kI8QTile;
+        __syncthreads();   // the previous tile's sigma / words are consumed
+        for (int p = tid; p < kI8QTile; p += blockDim.x) {
+            const int gp = pbase + p;
+            sh_sig[p] = gp < a.N ? a.sigma[(size_t)c * a.N + gp] : __int_as_float(0x7fc00000);
+        }
+        const int nvalid = a.N - pbase;   // pixels of this tile that exist (may exceed 128)
+        const float* Lr = a.L + ((size_t)c * a.N + pbase) * B + gr;
+        float lv[2][4][4];   // all 32 of this thread's radiances in flight at once
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int p = 4 * (q + 4 * (4 * h + u)) + k;
-                lv[u][k] = (band && p < nvalid) ? __ldg(Lr + (size_t)p * B) : 0.f;
-            }
+            for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int w = q + 4 * (4 * h + u);
-            int dgk[4][kI8S];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                float v = fmaf(-sh_sig[4 * w + k], beta, lv[u][k]) + gamma;
-                v = fabsf(v) <= 3.402823466e38f ? v : 0.f;
-                // q = rint(v 2^(27-e)), |q| < 2^27 (v 2^(27-e) is exact: a power-of-two scaling),
-                // then signed base-128 digits in [-64, 63] from the least significant one up:
-                // the low 7 bits sign-extended, and the exact quotient of the rest
-                int qi = __float2int_rn(v * sc);
-#pragma unroll
-                for (int d = kI8S - 1; d > 0; --d) {
-                    const int dd = (int)((unsigned)qi << 25) >> 25;
-                    dgk[k][d] = dd;
-                    qi = (qi - dd) >> 7;   // exact: qi - dd is a multiple of 128
+                for (int k = 0; k < 4; ++k) {
+                    const int p = 4 * (q + 4 * (4 * h + u)) + k;
+                    lv[h][u][k] = (band && p < nvalid) ? __ldg(Lr + (size_t)p * B) : 0.f;
                 }
-                dgk[k][0] = qi;   // |q| < 2^27 -> |s1| <= 64
-            }
+        __syncthreads();
 #pragma unroll
-            for (int d = 0; d < kI8S; ++d) {
-                const uint32_t lo = __byte_perm((uint32_t)dgk[0][d], (uint32_t)dgk[1][d], 0x0040);
-                const uint32_t hi = __byte_perm((uint32_t)dgk[2][d], (uint32_t)dgk[3][d], 0x0040);
-                qsm[(d * kI8QRows + r) * 33 + w] = __byte_perm(lo, hi, 0x5410);
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int w = q + 4 * (4 * h + u);
+                unsigned dgk[4][kI8S];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float v = fmaf(-sh_sig[4 * w + k], beta, lv[h][u][k]) + gamma;
+                    v = fabsf(v) <= 3.402823466e38f ? v : 0.f;
+                    // q = rint(v 2^(27-e)), |q| < 2^27 (v 2^(27-e) is exact: a power-of-two
+                    // scaling). Its signed base-128 digits d_k in [-64, 63] (top digit [-64, 64])
+                    // are the plain base-128 digits of q + 64 (1 + 2^7 + 2^14 + 2^21) minus 64 --
+                    // no carries -- so a digit is a shift and a mask, and the -64 is one
+                    // per-byte subtraction per word
+                    const unsigned qb = (unsigned)(__float2int_rn(v * sc) + 0x8102040);
+                    dgk[k][3] = qb & 127u;
+                    dgk[k][2] = (qb >> 7) & 127u;
+                    dgk[k][1] = (qb >> 14) & 127u;
+                    dgk[k][0] = qb >> 21;
+                }
+#pragma unroll
+                for (int d = 0; d < kI8S; ++d) {
+                    const uint32_t lo = __byte_perm(dgk[0][d], dgk[1][d], 0x0040);
+                    const uint32_t hi = __byte_perm(dgk[2][d], dgk[3][d], 0x0040);
+                    qsm[(d * kI8QRows + r) * 33 + w] = __vsub4(__byte_perm(lo, hi, 0x5410), 0x40404040u);
+                }
             }
-        }
-    }
-    __syncthreads();
-    // write out: warp = 8 (slice, row) pairs per pass, lane = word (128 B per row segment)
-    const int w = tid & 31, pw_lim = min(kI8QTile, a.Np - pbase) / 4;   // Np is a multiple of 16
-    if (w < pw_lim) {
-        const int nrows = min(kI8QRows, R - rbase);
-        for (int sr = tid >> 5; sr < kI8S * kI8QRows; sr += 8) {
-            const int s = sr / kI8QRows, rr = sr - s * kI8QRows;
-            if (rr >= nrows) continue;
-            uint32_t* dst = reinterpret_cast<uint32_t*>(a.slices + (((size_t)c * kI8S + s) * R + rbase + rr) * a.Np + pbase);
-            dst[w] = qsm[sr * 33 + w];
-        }
+        __syncthreads();
+        // write out: warp = 8 (slice, row) pairs per pass, lane = word (128 B per row segment)
+        const int w = tid & 31, pw_lim = min(kI8QTile, a.Np - pbase) / 4;   // Np is a multiple of 16
+        if (w < pw_lim)
+            for (int sr = tid >> 5; sr < kI8S * kI8QRows; sr += 8) {
+                const int s = sr / kI8QRows, rr = sr - s * kI8QRows;
+                if (rr >= nrows) continue;
+                uint32_t* dst =
+                    reinterpret_cast<uint32_t*>(a.slices + (((size_t)c * kI8S + s) * R + rbase + rr) * a.Np + pbase);
+                dst[w] = qsm[sr * 33 + w];
+            }
     }
 }
 
