@@ -1213,14 +1213,16 @@ __device__ inline double min_eig3(const double K[3][3]) {
     const double det = K[0][0] * (K[1][1] * K[2][2] - K[1][2] * K[2][1]) -
                        K[0][1] * (K[1][0] * K[2][2] - K[1][2] * K[2][0]) +
                        K[0][2] * (K[1][0] * K[2][1] - K[1][1] * K[2][0]);
-    // lambda^3 + a lambda^2 + b lambda + c = 0 with a = -tr, b = c2, c = -det
+    // lambda^3 + a lambda^2 + b lambda + c = 0 with a = -tr, b = c2, c = -det. The trigger
+    // compares the result with kLitTau = 1e-3 on an O(1) spectrum, so the trigonometric root
+    // is taken in fp32 (the coefficients stay fp64)
     const double a3 = -tr / 3.0;
     const double Q = a3 * a3 - c2 / 3.0;
     const double R = a3 * a3 * a3 - a3 * c2 / 2.0 - det / 2.0;
     if (!(Q > 0.0)) return isfinite(Q) ? -a3 : Q;   // triple root (or NaN)
-    const double sq = sqrt(Q);
-    const double x = fmin(1.0, fmax(-1.0, R / (Q * sq)));
-    return -2.0 * sq * cos(acos(x) / 3.0) - a3;
+    const float sq = sqrtf((float)Q);
+    const float x = fminf(1.f, fmaxf(-1.f, (float)(R / (Q * (double)sq))));
+    return (double)(-2.f * sq * cosf(acosf(x) * (1.f / 3.f))) - a3;
 }
 
 // lower-triangle packed index (i >= j)
