@@ -703,3 +703,25 @@ def test_nvtx_and_diagnostics_do_not_change_results(smf, torch):
     for e, a in outs[1:]:
         np.testing.assert_array_equal(e, outs[0][0])
         np.testing.assert_array_equal(a, outs[0][1])
+
+
+@pytest.mark.parametrize("bands", [32, 13])
+def test_literal_iteration_grouped_and_masked(smf, torch, bands):
+    """The literal covariance path (C16'') on pooled partitions (grouping) and with
+    nodata masking (censored pixels take no part; their alpha is NaN and skipped)."""
+    cfg = synth.scaled(synth.CONFIGS["tiny"], cols=5, pixels=300, bands=bands, rank=8)
+    cube, s, _ = synth.generate(cfg)
+    rng = np.random.default_rng(3)
+    for c in range(5):
+        cube[c, rng.choice(300, size=12, replace=False)] = -9999.0
+    # grouped, masked, literal on every iteration
+    r = smf.Retriever(bands, s, n_iter=6, group=2, nodata=-9999.0, cov_check="always")
+    enh, alb, st = r.retrieve(torch.from_numpy(np.ascontiguousarray(cube)).cuda())
+    assert r.synchronize(st) == -1
+    enh, alb = enh.cpu().numpy(), alb.cpu().numpy()
+    for c0, c1 in ((0, 2), (2, 4), (4, 5)):
+        part = cube[c0:c1].reshape(1, (c1 - c0) * 300, bands)
+        a_ref, r_ref, st_ref = oracle.retrieve_masked(part, s, -9999.0, n_iter=6)
+        assert st_ref[0] == 0
+        print(assert_parity(enh[c0:c1].reshape(-1), alb[c0:c1].reshape(-1), a_ref[0], r_ref[0],
+                            f"literal grouped+masked B={bands} {c0}:{c1}"))
