@@ -848,7 +848,10 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init smem attribute");
         {
             ProfScope ps(ctx, st, SMF_KERNEL_INIT);
-            k2w_init<<<p.cols, std::min(kWideNTI, (p.B + 31) / 32 * 32), p.smem2, st>>>(ia);
+            // a power of two of warps (the solves share each row among blockDim / 32 threads)
+            int nti = 32;
+            while (nti < kWideNTI && nti < p.B) nti *= 2;
+            k2w_init<<<p.cols, nti, p.smem2, st>>>(ia);
         }
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init launch");

@@ -208,64 +208,45 @@ __device__ bool wide_cholesky(double* A, int B, double tol, double* D, double* D
 }
 
 // y_r = x_r - sum_{cc in [cs, ce)} M[J0 + r][cc] x[cc] for the nb <= 32 rows of block J0 and NR
-// right-hand sides (x: shared [NR][B]); result in yv (shared [NR][32]). Threads stride the
-// columns (coalesced row segments, up to 16 rows' loads in flight per thread); a transpose-
-// reduction per 16 rows leaves row r's warp partial in one lane; red: shared [nwarps][NR][32].
+// right-hand sides (x: shared [NR][B]); result in yv (shared [NR][32]). blockDim.x / 32 threads
+// share a row (a warp covers 32 / tpr rows, the row segments it reads are 8 * tpr bytes wide);
+// each thread issues up to 32 of its row's loads at once, so a block step costs one or two
+// global round trips; the row's threads reduce with shuffles.
+#ifndef SMF_GEMV_BATCH
+#define SMF_GEMV_BATCH 16
+#endif
+constexpr int kGemvBatch = SMF_GEMV_BATCH;   // loads in flight per thread in the solves' GEMVs
+
 template <int NR>
 __device__ __forceinline__ void row_gemv(const double* __restrict__ M, int B, int J0, int nb, int cs, int ce,
-                                         const double* x, double* red, double* yv) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x, nw = nt >> 5;
-#pragma unroll 1
-    for (int rh = 0; rh < 2; ++rh) {
-        double acc[16][NR];
+                                         const double* x, double* /*red*/, double* yv) {
+    const int tid = threadIdx.x, tpr = blockDim.x >> 5;   // threads per row (4 or 8)
+    const int r = tid / tpr, cq = tid - r * tpr;
+    double acc[NR];
 #pragma unroll
-        for (int r = 0; r < 16; ++r)
+    for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+    const double* Mr = M + (size_t)(J0 + (r < nb ? r : 0)) * B;
+    for (int base = cs + cq; base < ce; base += kGemvBatch * tpr) {
+        double lv[kGemvBatch];
 #pragma unroll
-            for (int q = 0; q < NR; ++q) acc[r][q] = 0.0;
-        if (rh * 16 < nb) {
-            for (int cc = cs + tid; cc < ce; cc += nt) {
-                double lv[16];
-#pragma unroll
-                for (int r = 0; r < 16; ++r) {
-                    const int rr = rh * 16 + r;
-                    lv[r] = rr < nb ? M[(size_t)(J0 + rr) * B + cc] : 0.0;
-                }
-                double xv[NR];
-#pragma unroll
-                for (int q = 0; q < NR; ++q) xv[q] = x[q * B + cc];
-#pragma unroll
-                for (int r = 0; r < 16; ++r)
-#pragma unroll
-                    for (int q = 0; q < NR; ++q) acc[r][q] = fma(lv[r], xv[q], acc[r][q]);
-            }
+        for (int u = 0; u < kGemvBatch; ++u) {
+            const int cc = base + u * tpr;
+            lv[u] = (r < nb && cc < ce) ? Mr[cc] : 0.0;
         }
-        // transpose-reduce: after the halvings lane l holds row (l & 15)'s partial over the
-        // 16 lanes that share bit 4; the last xor adds the other half
 #pragma unroll
-        for (int q = 0; q < NR; ++q) {
+        for (int u = 0; u < kGemvBatch; ++u) {
+            const int cc = min(base + u * tpr, ce - 1);
 #pragma unroll
-            for (int off = 8; off >= 1; off >>= 1) {
-#pragma unroll
-                for (int i = 0; i < off; ++i) {
-                    const bool up = lane & off;
-                    const double send = up ? acc[i][q] : acc[i + off][q];
-                    const double keep = up ? acc[i + off][q] : acc[i][q];
-                    acc[i][q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-                }
-            }
-            acc[0][q] += __shfl_xor_sync(0xffffffffu, acc[0][q], 16);
-            if (lane < 16) red[(wid * NR + q) * 32 + rh * 16 + lane] = acc[0][q];
+            for (int q = 0; q < NR; ++q) acc[q] = fma(lv[u], x[q * B + cc], acc[q]);
         }
     }
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+        for (int off = 1; off < tpr; off <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+    if (cq == 0 && r < nb)
+#pragma unroll
+        for (int q = 0; q < NR; ++q) yv[q * 32 + r] = x[q * B + J0 + r] - acc[q];
     __syncthreads();
-    if (wid == 0 && lane < nb) {
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-            double s = 0.0;
-            for (int w = 0; w < nw; ++w) s += red[(w * NR + q) * 32 + lane];
-            yv[q * 32 + lane] = x[q * B + J0 + lane] - s;
-        }
-    }
 }
 
 // Stage diagonal block [J0, J0 + nb) of M (lower: L_JJ^-1, upper: its transpose) into Dsm.
