@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kWideNT1, 2) k1w_stats(WideStatsArgs a) {
 
 // ---------------------------------------------------------------- K2w init
 constexpr int kWideNT2 = 128;    // k2w_update threads (5 CTAs per SM: one wave of 598 columns)
-constexpr int kWideNTI = 256;     // k2w_init threads (1 CTA per SM: up to 255 registers for the register-resident diagonal factor)
+constexpr int kWideNTI = 512;     // k2w_init threads (1 CTA per SM)
 
 struct WideInitArgs {
     ColState cs;

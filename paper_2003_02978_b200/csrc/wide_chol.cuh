@@ -58,16 +58,24 @@ __device__ bool chol_diag_warp(const double* A, int B, int k0, int nb, double to
     for (int m = 0; m < kChB; ++m) D[lane * kChD + m] = r[m];
     __syncwarp();
     if (ok) {
+        // column `lane` of L_KK^-1 by right-looking substitution: once x_k is final, every
+        // later x_i takes its update at once (independent FMAs; the dependent chain is 32
+        // steps, not the 500 of a dot product per entry)
+        Dinv[lane * kChD + lane] = lane < nb ? 1.0 / D[lane * kChD + lane] : 0.0;   // reciprocal pivots
+        __syncwarp();
         double x[kChB];
 #pragma unroll
-        for (int i = 0; i < kChB; ++i) {
-            double v = i == lane ? 1.0 : 0.0;
+        for (int i = 0; i < kChB; ++i) x[i] = i == lane ? 1.0 : 0.0;
 #pragma unroll
-            for (int k = 0; k < i; ++k) v = fma(-D[i * kChD + k], x[k], v);
-            x[i] = i < nb ? v * (1.0 / D[i * kChD + i]) : 0.0;
+        for (int k = 0; k < kChB; ++k) {
+            const double xk = x[k] * Dinv[k * kChD + k];
+            x[k] = xk;
+#pragma unroll
+            for (int i = k + 1; i < kChB; ++i) x[i] = fma(-D[i * kChD + k], xk, x[i]);
         }
+        __syncwarp();
 #pragma unroll
-        for (int i = 0; i < kChB; ++i) Dinv[i * kChD + lane] = x[i];
+        for (int i = 0; i < kChB; ++i) Dinv[i * kChD + lane] = i < nb ? x[i] : 0.0;
     }
     __syncwarp();
     return ok;
