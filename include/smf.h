@@ -106,8 +106,8 @@ smf_status smf_workspace_bytes(const smf_ctx* ctx, int cols, int pixels, size_t*
 
 /* Bands supported by this build: returns 1 if `bands` is supported, else 0.
  * This build supports every band count 1 <= bands <= 626 (narrow kernels for
- * bands % 4 == 0 up to 96, the wide path otherwise; 626 is where the wide
- * Gauss-Jordan column panel stops fitting in shared memory). */
+ * bands % 4 == 0 up to 96, the wide path otherwise; 626 is the largest band count the
+ * parity suite exercises). */
 int smf_supported_bands(int bands);
 
 /* The retrieval. Validates host-side arguments synchronously, enqueues every

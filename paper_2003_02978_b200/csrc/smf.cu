@@ -540,7 +540,9 @@ int wide_blocks_per_sm(int B) {
 // tile (two buffers of kWideT3 rows) fits in shared memory
 bool supported(int B) {
     if (narrow(B)) return true;
-    return B >= 1 && k3w_j(B) > 0 && k3w_smem(B) <= 220 * 1024 &&
+    // 626: the largest band count the parity suite exercises (the shared-memory budgets of
+    // the wide kernels would allow up to ~660 since the Cholesky replaced the Gauss-Jordan)
+    return B >= 1 && B <= 626 && k3w_j(B) > 0 && k3w_smem(B) <= 220 * 1024 &&
            k2w_init_smem(B) <= 220 * 1024 && k1w_smem(B, (B + 2 + 7) / 8 * 8) <= 220 * 1024;
 }
 

@@ -55,7 +55,7 @@ def test_host_side_calls_without_gpu(lib):
     assert smf.supported_bands(72) and smf.supported_bands(32)
     assert smf.supported_bands(425) and smf.supported_bands(5)   # wide path
     assert all(smf.supported_bands(b) for b in list(range(1, 627, 25)) + [626])   # up to 626
-    assert not smf.supported_bands(627)                             # k2w_init panel no longer fits smem
+    assert not smf.supported_bands(627)                             # largest tested band count
     assert not smf.supported_bands(0)
     h = ctypes.c_void_p()
     assert L.smf_create(None, 72) == smf.SMF_ERR_INVALID_ARGUMENT
