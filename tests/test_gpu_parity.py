@@ -725,3 +725,67 @@ def test_literal_iteration_grouped_and_masked(smf, torch, bands):
         assert st_ref[0] == 0
         print(assert_parity(enh[c0:c1].reshape(-1), alb[c0:c1].reshape(-1), a_ref[0], r_ref[0],
                             f"literal grouped+masked B={bands} {c0}:{c1}"))
+
+
+def test_wide_int8_statistics_multi_run_partition(smf, torch):
+    """A pooled wide partition longer than one int32 run of the int8 SYRK (131 072 pixels:
+    the digit products' overflow bound) -- the runs are folded into the fp64 partial
+    (all-columns grouping). C0 against the oracle on the pooled rows, and parity."""
+    cols, pixels, bands = 3, 50000, 13
+    cfg = synth.scaled(synth.CONFIGS["tiny"], cols=cols, pixels=pixels, bands=bands, rank=8)
+    cube, s, _ = synth.generate(cfg)
+    pooled = cube.reshape(1, cols * pixels, bands)
+    r = smf.Retriever(bands, s, n_iter=4, group=cols)
+    enh, alb, st = r.retrieve(torch.from_numpy(np.ascontiguousarray(cube)).cuda())
+    assert r.synchronize(st) == -1
+    a_ref, r_ref, rc = oracle.retrieve_column(pooled[0], s, n_iter=4)
+    assert rc == 0
+    print(assert_parity(enh.cpu().numpy().reshape(-1), alb.cpu().numpy().reshape(-1), a_ref, r_ref,
+                        "wide pooled 150000 px"))
+    r1 = smf.Retriever(bands, s)
+    mean, cov = r1.initial_statistics(torch.from_numpy(np.ascontiguousarray(pooled)).cuda())
+    C_ref = oracle.covariance(pooled[0])
+    scale = np.sqrt(np.outer(np.diag(C_ref), np.diag(C_ref)))
+    err = (np.abs(cov.cpu().numpy()[0] - C_ref) / scale).max()
+    print("pooled int8 C0 max rel err", err)
+    # three columns' spectra pooled: the first column's pilot leaves the shifted rows far from
+    # zero mean, so C0 = S/N - m m^T cancels more than within one column (5.4e-8 measured)
+    assert err < 2e-7
+
+
+def test_retrieve_argument_errors(smf, torch):
+    """Empty and malformed inputs fail synchronously with typed status codes, enqueue nothing
+    and leave the context usable (include/smf.h error contract)."""
+    import ctypes
+    L = smf._lib
+    cfg = synth.scaled(synth.CONFIGS["tiny"], cols=2, pixels=64, bands=32)
+    cube, s, _ = synth.generate(cfg)
+    rad = torch.from_numpy(cube).cuda()
+    r = smf.Retriever(32, s, n_iter=2)
+    ws = r.alloc_workspace(2, 64)
+    enh = torch.empty((2, 64), device="cuda")
+    alb = torch.empty_like(enh)
+    st = torch.empty(2, dtype=torch.int32, device="cuda")
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    E = smf.SMF_ERR_INVALID_ARGUMENT
+    assert L.smf_retrieve(r._h, P(rad), 0, 64, P(enh), P(alb), P(ws), P(st), stream) == E          # no columns
+    assert L.smf_retrieve(r._h, P(rad), 2, 1, P(enh), P(alb), P(ws), P(st), stream) == E           # < 2 pixels
+    assert L.smf_retrieve(r._h, None, 2, 64, P(enh), P(alb), P(ws), P(st), stream) == E            # NULL cube
+    assert L.smf_retrieve(r._h, P(rad), 2, 64, P(enh), P(enh), P(ws), P(st), stream) == E          # aliased outputs
+    assert L.smf_retrieve(r._h, P(rad), 2, 64, P(rad), P(alb), P(ws), P(st), stream) == E          # output = input
+    mis = ctypes.c_void_p(rad.data_ptr() + 4)   # narrow path: TMA needs a 16-byte aligned cube
+    assert L.smf_retrieve(r._h, mis, 1, 64, P(enh), P(alb), P(ws), P(st), stream) == E
+    wsm = ctypes.c_void_p(ws.data_ptr() + 8)    # workspace must be 256-byte aligned
+    assert L.smf_retrieve(r._h, P(rad), 2, 64, P(enh), P(alb), wsm, P(st), stream) == E
+    h = ctypes.c_void_p()
+    assert L.smf_create(ctypes.byref(h), 32) == smf.SMF_OK
+    assert L.smf_retrieve(h, P(rad), 2, 64, P(enh), P(alb), P(ws), P(st), stream) == smf.SMF_ERR_NOT_CONFIGURED
+    L.smf_destroy(h)
+    with pytest.raises(smf.SMFError):
+        r.retrieve(torch.zeros((2, 64, 16), device="cuda"))                                      # bands mismatch
+    with pytest.raises(smf.SMFError):
+        smf.Retriever(32, s, n_iter=-1)
+    # the context still works
+    enh2, alb2, st2 = r.retrieve(rad, enh, alb, ws, st)
+    assert r.synchronize(st2) == -1 and np.isfinite(enh2.cpu().numpy()).all()
