@@ -264,7 +264,7 @@ bool make_plan(const smf_ctx* ctx, int cols, int N, Plan& p) {
     p.o_mu = take(cb * 8);
     p.o_tprev = take(cb * 8);
     p.o_yprev = take(cb * 8);
-    p.o_ainv = take(cb * B * 8);
+    p.o_ainv = take(cb * (p.wide ? wide_ld(B) : B) * 8);   // wide: the factor's rows padded to an even stride
     p.o_q64 = take((size_t)cols * 8);
     p.o_z32 = take(cb * 4);
     p.o_mhat = take(cb * 4);

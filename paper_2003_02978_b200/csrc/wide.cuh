@@ -226,10 +226,10 @@ struct WideInitArgs {
     double ridge_rel;
 };
 
-// shared: dm, srx, cv, vt, mh [B]; D, Dinv [32][33]; the panel Cp [B][34] (after the
+// shared: dm, srx, cv, vt, mh [B]; D, Dinv [32][33]; the panel Cp [B][32] (after the
 // factorisation reused for the solves: x [2][B], red [16][2][32], yv [2][32]); scratch [32][4]
 __host__ __device__ inline size_t k2w_init_panel(int B) {
-    const size_t p = (size_t)B * (kChB + 2), q = (size_t)2 * B + 16 * 2 * 32 + 2 * 32;
+    const size_t p = (size_t)B * kChB, q = (size_t)2 * B + 16 * 2 * 32 + 2 * 32;
     return p > q ? p : q;
 }
 __host__ inline size_t k2w_init_smem(int B) { return (size_t)(5 * B + 2 * kChB * kChD + k2w_init_panel(B) + 32 * 4) * 8 + 32; }
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     double* mh = vt + B;         // [B] fp32 mhat (as double)
     double* D = mh + B;          // [kChB][kChD] diagonal block
     double* Dinv = D + kChB * kChD;                  // [kChB][kChD] its inverse
-    double* Cp = Dinv + kChB * kChD + ((5 * B) & 1);   // [B][kChB + 2] panel (16-byte aligned)
+    double* Cp = Dinv + kChB * kChD + ((5 * B) & 1);   // [B][kChB] panel (16-byte aligned)
     double* scratch = Cp + k2w_init_panel(B);   // [32][4]
     __shared__ int bad, chol_flag;
     __shared__ double sh_tol, sh_mm;
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
         if (!a.sym && (i >> 7) == (k >> 7)) return 0.5 * (S[(size_t)i * BEp + k] + S[(size_t)k * BEp + i]);
         return S[(size_t)i * BEp + k];
     };
-    double* A = a.cs.ainv + (size_t)c * B * B;
+    double* A = a.cs.ainv + (size_t)c * B * wide_ld(B);   // row stride wide_ld(B)
     if (tid == 0) bad = COL_OK;
     __syncthreads();
     const double Nv = a.cs.mask ? ext(B + 1, B + 1) : (double)a.N;   // valid rows when masking
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
         const double s2 = ext(i, k) + srx[i] * cv[k] + cv[i] * srx[k] + Srr * cv[i] * cv[k];
         const double v = s2 * invN - dm[i] * dm[k];
         if (!isfinite(v)) nonfinite = 1;
-        A[(size_t)i * B + k] = v;   // lower triangle only (the Cholesky reads nothing else)
+        A[(size_t)i * wide_ld(B) + k] = v;   // lower triangle only (the Cholesky reads nothing else)
         if (a.cov_out) {
             a.cov_out[(size_t)c * B * B + (size_t)i * B + k] = v;
             a.cov_out[(size_t)c * B * B + (size_t)k * B + i] = v;
@@ -307,15 +307,15 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     __syncthreads();
     {
         double loc[1] = {0.0};   // trace
-        for (int b = tid; b < B; b += nt) loc[0] += A[(size_t)b * B + b];
+        for (int b = tid; b < B; b += nt) loc[0] += A[(size_t)b * wide_ld(B) + b];
         block_sum<1>(loc, scratch);
         if (tid == 0) {
             const double rho = a.ridge_rel * loc[0] / (double)B;
             a.cs.rho64[c] = rho;
             double amax = 0.0;
             for (int b = 0; b < B; ++b) {
-                A[(size_t)b * B + b] += rho;
-                amax = fmax(amax, A[(size_t)b * B + b]);
+                A[(size_t)b * wide_ld(B) + b] += rho;
+                amax = fmax(amax, A[(size_t)b * wide_ld(B) + b]);
             }
             sh_tol = (double)B * 2.220446049250313e-16 * amax;
         }
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a) {
     __shared__ int sh_st, sh_lit;
     ColState& cs = a.cs;
     if (cs.status[c] != COL_OK) return;   // uniform per block
-    const double* Lf = cs.ainv + (size_t)c * B * B;   // Cholesky factor (lower, row-major)
+    const double* Lf = cs.ainv + (size_t)c * B * wide_ld(B);   // the solve-ready factor (row stride wide_ld(B))
     // 1. sufficient statistics of the previous sweep (fixed CTA order)
     const long long c0 = (long long)c * a.tpc, c1 = c0 + a.tpc;
     int b0 = (int)((c0 * a.G) / a.ttot);

@@ -25,6 +25,9 @@
 namespace smf {
 
 constexpr int kChB = 32;         // block width of the factorisation and the solves
+// row stride of the stored factor: even, so every row is 16-byte aligned (the solves read
+// row segments as double2)
+__host__ __device__ inline int wide_ld(int B) { return (B + 1) & ~1; }
 constexpr int kChD = kChB + 1;   // padded row stride of the shared diagonal block
 
 // Factor and invert the diagonal block at k0 (nb <= 32 rows) by the calling warp: stage
@@ -35,7 +38,7 @@ __device__ bool chol_diag_warp(const double* A, int B, int k0, int nb, double to
     const int lane = threadIdx.x & 31;
     double r[kChB];
 #pragma unroll
-    for (int m = 0; m < kChB; ++m) r[m] = (lane < nb && m <= lane) ? A[(size_t)(k0 + lane) * B + k0 + m] : 0.0;
+    for (int m = 0; m < kChB; ++m) r[m] = (lane < nb && m <= lane) ? A[(size_t)(k0 + lane) * wide_ld(B) + k0 + m] : 0.0;
     bool ok = true;
 #pragma unroll
     for (int j = 0; j < kChB; ++j) {
@@ -81,10 +84,15 @@ __device__ bool chol_diag_warp(const double* A, int B, int k0, int nb, double to
     return ok;
 }
 
+// The panel Cp holds row r's 32 values as 16 double2 pairs, pair s2 at slot s2 ^ cp_swz(r): the
+// trailing tiles of a warp read rows 4 apart (tile columns J, J + 1, ...), which an unswizzled
+// stride maps onto the same banks.
+__device__ __forceinline__ int cp_swz(int r) { return (r >> 2) & 7; }
+
 // 4 x 4 register tile (I, J) of the trailing update A_ij -= Cp_i . Cp_j (j <= i) below row
-// and right of column t0 (tile rows t0 + 4I.., columns t0 + 4J..).
+// and right of column t0 (tile rows t0 + 4I.., columns t0 + 4J..; t0 is a multiple of 4, so
+// a tile's four rows share one swizzle).
 __device__ __forceinline__ void chol_tile(double* A, int B, int t0, int I, int J, const double* Cp) {
-    constexpr int CS = kChB + 2;
     const int i0 = t0 + 4 * I, j0 = t0 + 4 * J;
     double acc[4][4];
 #pragma unroll
@@ -95,24 +103,25 @@ __device__ __forceinline__ void chol_tile(double* A, int B, int t0, int I, int J
     const double2* rj[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        ri[q] = reinterpret_cast<const double2*>(Cp + min(i0 + q, B - 1) * CS);
-        rj[q] = reinterpret_cast<const double2*>(Cp + min(j0 + q, B - 1) * CS);
+        ri[q] = reinterpret_cast<const double2*>(Cp + min(i0 + q, B - 1) * kChB);
+        rj[q] = reinterpret_cast<const double2*>(Cp + min(j0 + q, B - 1) * kChB);
     }
+    const int dg = cp_swz(i0) ^ cp_swz(j0);   // slot p of row i pairs with slot p ^ dg of row j
     double old[4][4];   // the 16 old values in flight while the products accumulate
 #pragma unroll
     for (int a2 = 0; a2 < 4; ++a2)
 #pragma unroll
         for (int b2 = 0; b2 < 4; ++b2) {
             const int i = i0 + a2, j = j0 + b2;
-            old[a2][b2] = (i < B && j <= i) ? A[(size_t)i * B + j] : 0.0;
+            old[a2][b2] = (i < B && j <= i) ? A[(size_t)i * wide_ld(B) + j] : 0.0;
         }
 #pragma unroll 4
-    for (int s2 = 0; s2 < kChB / 2; ++s2) {
+    for (int p = 0; p < kChB / 2; ++p) {
         double2 va[4], vb[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            va[q] = ri[q][s2];
-            vb[q] = rj[q][s2];
+            va[q] = ri[q][p];
+            vb[q] = rj[q][p ^ dg];
         }
 #pragma unroll
         for (int a2 = 0; a2 < 4; ++a2)
@@ -125,7 +134,7 @@ __device__ __forceinline__ void chol_tile(double* A, int B, int t0, int I, int J
 #pragma unroll
         for (int b2 = 0; b2 < 4; ++b2) {
             const int i = i0 + a2, j = j0 + b2;
-            if (i < B && j <= i) A[(size_t)i * B + j] = old[a2][b2] - acc[a2][b2];
+            if (i < B && j <= i) A[(size_t)i * wide_ld(B) + j] = old[a2][b2] - acc[a2][b2];
         }
 }
 
@@ -142,10 +151,9 @@ __device__ __forceinline__ void tri_decode(int e, int& I, int& J) {
 //   diagonal blocks: lower (incl. diagonal) L_KK^-1, strictly upper (L_KK^-1)^T.
 // Look-ahead: once the trailing update has finished the next block column, warp 0 factors
 // the next diagonal block while the other warps apply the rest of the trailing update.
-// D, Dinv: shared [kChB][kChD]; Cp: shared [B][kChB + 2] (16-byte aligned rows); flag:
+// D, Dinv: shared [kChB][kChD]; Cp: shared [B][kChB] (16-byte aligned, swizzled pairs); flag:
 // shared int. Returns false (uniformly) on a non-positive or non-finite pivot (<= tol).
 __device__ bool wide_cholesky(double* A, int B, double tol, double* D, double* Dinv, double* Cp, int* flag) {
-    constexpr int CS = kChB + 2;
     const int tid = threadIdx.x, nt = blockDim.x, wid = tid >> 5;
     if (tid == 0) *flag = 0;
     __syncthreads();
@@ -157,13 +165,13 @@ __device__ bool wide_cholesky(double* A, int B, double tol, double* D, double* D
         // (a) the factored block (D, Dinv) is final: write L_KK^-1 and its transpose
         for (int e = tid; e < nb * nb; e += nt) {
             const int r = e / nb, cc = e - r * nb;
-            A[(size_t)(k0 + r) * B + k0 + cc] = cc <= r ? Dinv[r * kChD + cc] : Dinv[cc * kChD + r];
+            A[(size_t)(k0 + r) * wide_ld(B) + k0 + cc] = cc <= r ? Dinv[r * kChD + cc] : Dinv[cc * kChD + r];
         }
         // (b) panel: x = a L_KK^-T for every row below the block (thread per row), staged in
         // Cp, written to the lower part and mirrored (L^T) into the upper part
         for (int i = k0 + nb + tid; i < B; i += nt) {
             double a_[kChB];
-            double* Ai = A + (size_t)i * B + k0;
+            double* Ai = A + (size_t)i * wide_ld(B) + k0;
 #pragma unroll
             for (int s = 0; s < kChB; ++s) a_[s] = s < nb ? Ai[s] : 0.0;
 #pragma unroll
@@ -173,9 +181,9 @@ __device__ bool wide_cholesky(double* A, int B, double tol, double* D, double* D
 #pragma unroll
                     for (int t = 0; t <= s; ++t) v = fma(a_[t], Dinv[s * kChD + t], v);
                     Ai[s] = v;
-                    A[(size_t)(k0 + s) * B + i] = v;
+                    A[(size_t)(k0 + s) * wide_ld(B) + i] = v;
                 }
-                Cp[i * CS + s] = v;   // zero past nb
+                Cp[i * kChB + (((s >> 1) ^ cp_swz(i)) << 1) + (s & 1)] = v;   // zero past nb
             }
         }
         __syncthreads();
@@ -223,7 +231,8 @@ __device__ bool wide_cholesky(double* A, int B, double tol, double* D, double* D
 #ifndef SMF_GEMV_BATCH
 #define SMF_GEMV_BATCH 16
 #endif
-constexpr int kGemvBatch = SMF_GEMV_BATCH;   // loads in flight per thread in the solves' GEMVs
+constexpr int kGemvBatch = SMF_GEMV_BATCH;   // doubles in flight per thread in the solves' GEMVs
+constexpr int kGemvPairs = kGemvBatch / 2;   // ... loaded as double2 pairs
 
 template <int NR>
 __device__ __forceinline__ void row_gemv(const double* __restrict__ M, int B, int J0, int nb, int cs, int ce,
@@ -233,19 +242,24 @@ __device__ __forceinline__ void row_gemv(const double* __restrict__ M, int B, in
     double acc[NR];
 #pragma unroll
     for (int q = 0; q < NR; ++q) acc[q] = 0.0;
-    const double* Mr = M + (size_t)(J0 + (r < nb ? r : 0)) * B;
-    for (int base = cs + cq; base < ce; base += kGemvBatch * tpr) {
-        double lv[kGemvBatch];
+    // rows are 16-byte aligned (wide_ld): each load fetches a column pair (cc, cc + 1), cc even
+    const double* Mr = M + (size_t)(J0 + (r < nb ? r : 0)) * wide_ld(B);
+    const int cs2 = cs & ~1;
+    for (int base = cs2 + 2 * cq; base < ce; base += 2 * kGemvPairs * tpr) {
+        double2 lv[kGemvPairs];
 #pragma unroll
-        for (int u = 0; u < kGemvBatch; ++u) {
-            const int cc = base + u * tpr;
-            lv[u] = (r < nb && cc < ce) ? Mr[cc] : 0.0;
+        for (int u = 0; u < kGemvPairs; ++u) {
+            const int cc = base + 2 * u * tpr;
+            lv[u] = (r < nb && cc < ce) ? *reinterpret_cast<const double2*>(Mr + cc) : make_double2(0.0, 0.0);
         }
 #pragma unroll
-        for (int u = 0; u < kGemvBatch; ++u) {
-            const int cc = min(base + u * tpr, ce - 1);
+        for (int u = 0; u < kGemvPairs; ++u) {
+            const int cc = base + 2 * u * tpr;
+            const bool ok0 = cc >= cs && cc < ce, ok1 = cc + 1 >= cs && cc + 1 < ce;
+            const double l0 = ok0 ? lv[u].x : 0.0, l1 = ok1 ? lv[u].y : 0.0;
+            const int c0 = ok0 ? cc : 0, c1 = ok1 ? cc + 1 : 0;
 #pragma unroll
-            for (int q = 0; q < NR; ++q) acc[q] = fma(lv[u], x[q * B + cc], acc[q]);
+            for (int q = 0; q < NR; ++q) acc[q] = fma(l1, x[q * B + c1], fma(l0, x[q * B + c0], acc[q]));
         }
     }
 #pragma unroll
@@ -261,7 +275,7 @@ __device__ __forceinline__ void row_gemv(const double* __restrict__ M, int B, in
 __device__ __forceinline__ void stage_diag(const double* __restrict__ M, int B, int J0, int nb, double* Dsm) {
     for (int e = threadIdx.x; e < kChB * kChB; e += blockDim.x) {
         const int i = e >> 5, l = e & 31;
-        Dsm[i * kChD + l] = (i < nb && l < nb) ? M[(size_t)(J0 + i) * B + J0 + l] : 0.0;
+        Dsm[i * kChD + l] = (i < nb && l < nb) ? M[(size_t)(J0 + i) * wide_ld(B) + J0 + l] : 0.0;
     }
 }
 
