@@ -574,6 +574,19 @@ CUresult make_maps(const float* rad, int cols, int N, int B, CUtensorMap* main_m
     return r;
 }
 
+// The wide path's solve-ready factor [cols][B][wide_ld(B)] fp64 as a 3-D map {B, B, cols} with
+// 32 x 32 boxes (rows/columns past B zero-filled) for k2w_update's streamed solves.
+CUresult make_factor_map(const double* f, int cols, int B, CUtensorMap* map) {
+    cuuint64_t dims[3] = {(cuuint64_t)B, (cuuint64_t)B, (cuuint64_t)cols};
+    cuuint64_t strides[2] = {(cuuint64_t)wide_ld(B) * 8, (cuuint64_t)B * wide_ld(B) * 8};
+    cuuint32_t box[3] = {(cuuint32_t)kChB, (cuuint32_t)kChB, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    memset(map, 0, sizeof(CUtensorMap));
+    return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)f, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
 ColState col_state(const Plan& p, unsigned char* ws, const float* s, const smf_ctx* ctx) {
     ColState cs;
     cs.mbar = (double*)(ws + p.o_mbar);
@@ -1333,6 +1346,14 @@ static smf_status retrieve_eager(smf_ctx* ctx, const float* radiance, int cols, 
     ua.r_floor = (float)ctx->r_floor;
     ua.use_albedo = ctx->use_albedo;
     ua.lit_mode = ctx->lit_mode;
+    CUtensorMap fmap;   // wide: the solve-ready factor, streamed by k2w_update's solves
+    if (p.wide) {
+        CUresult cr = make_factor_map(cs.ainv, cols, p.B, &fmap);
+        if (cr != CUDA_SUCCESS) {
+            set_err(ctx, "cuTensorMapEncodeTiled (factor) failed (%d)", (int)cr);
+            return SMF_ERR_CUDA;
+        }
+    }
     DiagArgs da;
     da.enh = enhancement;
     da.cs = cs;
@@ -1354,7 +1375,7 @@ static smf_status retrieve_eager(smf_ctx* ctx, const float* radiance, int cols, 
             {
                 ProfScope ps(ctx, st, SMF_KERNEL_UPDATE);
                 if (p.wide)
-                    k2w_update<<<cols, kWideNT2, smem_up, st>>>(ua);
+                    k2w_update<<<cols, kWideNT2, smem_up, st>>>(ua, fmap);
                 else {
                     void* args[] = {(void*)&ua};
                     e0 = launch_pdl(reinterpret_cast<const void*>(&k2_update), dim3(cols), dim3(128), args, smem_up,

@@ -395,11 +395,13 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
 }
 
 // ---------------------------------------------------------------- K2w update
-// shared: t [B], x_f [2][B] (forward: t, h -> L^-1 t, L^-1 h), x_b [1 or 4][B] (backward
-// right-hand sides; 4 with the energy trace), diagonal block [32][33], reduction
-// [nwarps][2][32], yv [2][32], scratch [32][18]
+// shared: t [B], x_f [2][B] (forward: t, h -> L^-1 t, L^-1 h), with the energy trace x_b [4][B]
+// (backward right-hand sides; otherwise the one backward right-hand side replaces w_t in x_f),
+// yv [4][32], scratch [96], then (128-byte aligned) the factor ring [kTsS][32][32] of the
+// streamed solves (wide_chol.cuh; 44.9 KB in all at B = 425: five CTAs per SM), which the
+// literal path reuses as the diagonal block [32][33] and reduction [4][2][32] of tri_fwd
 __host__ inline size_t k2w_update_smem(int B, int energy) {
-    return (size_t)((energy ? 7 : 4) * B + kChB * kChD + 4 * 2 * 32 + 2 * 32 + 32 * 18) * 8;
+    return (size_t)((energy ? 7 : 3) * B + 4 * 32 + 96 + 16 + kTsS * kTileD) * 8;
 }
 constexpr int kLitRows = 32;   // residual rows per chunk of the wide literal check
 // doubles of global scratch per column for the wide literal check (packed C^k + residual rows)
@@ -409,21 +411,29 @@ __host__ inline long long lit_doubles(int B) { return (long long)B * (B + 1) / 2
 // W = L^-1 U with U = [t', t, h] (w' = L^-1 t' kept from the previous update in yprev), G =
 // U^T A0^-1 U = W^T W, coef = M (I + G M)^-1 W^T w_t, z = L^-T (w_t - W coef). The energy trace
 // also needs Y = A0^-1 U = L^-T W (three more backward right-hand sides, same pass over L).
-__global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a) {
+__global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a, const __grid_constant__ CUtensorMap fmap) {
     extern __shared__ double w3_smem[];
     const int B = a.B, tid = threadIdx.x, c = blockIdx.x, nt = blockDim.x;
     double* sh_t = w3_smem;          // [B] t^k
     double* xf = sh_t + B;           // [2][B]
-    double* xb = xf + 2 * B;         // [4][B]
-    double* Dsm = xb + (a.energy_on ? 4 : 1) * B;   // [32][33]
-    double* red = Dsm + kChB * kChD; // [4][2][32]
-    double* yv = red + 4 * 2 * 32;   // [2][32]
-    double* scratch = yv + 2 * 32;   // [32][18]
-    __shared__ double sh_coef[3], sh_s[3];
+    // backward right-hand sides: [4][B] with the energy trace, else in place of w_t (xf[0..B))
+    double* xb = a.energy_on ? xf + 2 * B : xf;
+    double* yv = xf + (a.energy_on ? 6 : 2) * B;   // [4][32]
+    double* scratch = yv + 4 * 32;   // [96]: block_sum [4 warps][<= 18], literal check [32][3]
+    double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(scratch + 96) + 127) & ~(uintptr_t)127);
+    __shared__ double sh_coef[3], sh_s[3], sh_g[9];
     __shared__ int sh_st, sh_lit;
+    __shared__ __align__(8) uint64_t ts_full[kTsS], ts_empty[kTsS];
     ColState& cs = a.cs;
     if (cs.status[c] != COL_OK) return;   // uniform per block
     const double* Lf = cs.ainv + (size_t)c * B * wide_ld(B);   // the solve-ready factor (row stride wide_ld(B))
+    // the factor stream (forward then backward pass) starts before the statistics gather
+    TileStream ts;
+    ts_init(ts, ring, ts_full, ts_empty, &fmap, B, c, 2);
+    if (tid == 0) {
+        prefetch_tmap(&fmap);
+        ts_issue(ts, kTsS);
+    }
     // 1. sufficient statistics of the previous sweep (fixed CTA order)
     const long long c0 = (long long)c * a.tpc, c1 = c0 + a.tpc;
     int b0 = (int)((c0 * a.G) / a.ttot);
@@ -464,10 +474,10 @@ __global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a) {
     }
     __syncthreads();
     // 2. W = L^-1 [t, h]; 3. G = W^T W with W = [w', w_t, w_h] (U^T A0^-1 U)
-    tri_fwd<2>(Lf, B, xf, Dsm, red, yv);
-    double gv[18];   // G (9) and, with the energy trace, YY = Y^T Y (9, filled after the backward pass)
+    tri_stream<2, true>(ts, B, xf, yv);
+    double gv[9];   // G = W^T W (kept in shared memory for the energy trace's YY step)
 #pragma unroll
-    for (int i = 0; i < 18; ++i) gv[i] = 0.0;
+    for (int i = 0; i < 9; ++i) gv[i] = 0.0;
     for (int j = tid; j < B; j += nt) {
         const size_t o = (size_t)c * B + j;
         const double w[3] = {cs.yprev[o], xf[j], xf[B + j]};
@@ -478,8 +488,9 @@ __global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a) {
 #pragma unroll
             for (int q2 = 0; q2 < 3; ++q2) gv[r * 3 + q2] += w[r] * w[q2];
     }
-    block_sum<9>(*reinterpret_cast<double(*)[9]>(gv), scratch);
+    block_sum<9>(gv, scratch);
     if (tid == 0) {
+        for (int i = 0; i < 9; ++i) sh_g[i] = gv[i];
         // C^k = C0 + U M U^T, M in the basis (t', t, h)
         const double M[3][3] = {{bbar * bbar, -bbar * bbar, 0.0}, {-bbar * bbar, b2, -1.0}, {0.0, -1.0, 0.0}};
         double K[3][3], v[3], x[3];
@@ -505,7 +516,12 @@ __global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a) {
     __syncthreads();
     if (sh_lit) {
         // lines 10-16 literally (reading C16''), C^k and the residual rows in global scratch;
-        // then w' = L^-1 t^k for the next Woodbury update
+        // then w' = L^-1 t^k for the next Woodbury update (the prefetched backward tiles are
+        // drained first: the ring becomes tri_fwd's diagonal block and reduction buffer)
+        ts_drain(ts);
+        __syncthreads();
+        double* Dsm = ring;                 // [32][33]
+        double* red = ring + kChB * kChD;   // [4][2][32]
         double* Cp = a.lit + (size_t)c * a.lit_stride;
         const int stl = literal_iteration(a, c, nullptr, Cp, Cp + (size_t)B * (B + 1) / 2, kLitRows, xf, scratch);
         if (stl != COL_NOT_SPD) {
@@ -524,6 +540,7 @@ __global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a) {
     const int nr = a.energy_on ? 4 : 1;
     for (int j = tid; j < B; j += nt) {
         const double wp = cs.yprev[(size_t)c * B + j], wt = xf[j], wh = xf[B + j];
+        cs.yprev[(size_t)c * B + j] = wt;   // w' = L^-1 t for the next update
         xb[j] = wt - (wp * sh_coef[0] + wt * sh_coef[1] + wh * sh_coef[2]);
         if (nr == 4) {
             xb[B + j] = wp;
@@ -532,12 +549,10 @@ __global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a) {
         }
     }
     __syncthreads();
-    if (nr == 4) {
-        tri_bwd<2>(Lf, B, xb, Dsm, red, yv);
-        tri_bwd<2>(Lf, B, xb + 2 * B, Dsm, red, yv);
-    } else {
-        tri_bwd<1>(Lf, B, xb, Dsm, red, yv);
-    }
+    if (nr == 4)
+        tri_stream<4, false>(ts, B, xb, yv);
+    else
+        tri_stream<1, false>(ts, B, xb, yv);
     if (a.energy_on) {
         double yy[9];
 #pragma unroll
@@ -552,7 +567,7 @@ __global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a) {
         block_sum<9>(yy, scratch);
         if (tid == 0) {
             const double M[3][3] = {{bbar * bbar, -bbar * bbar, 0.0}, {-bbar * bbar, b2, -1.0}, {0.0, -1.0, 0.0}};
-            cs.tq[c] = woodbury_trace(M, gv, yy, B, cs.rho64[c], cs.tra[c], bbar);
+            cs.tq[c] = woodbury_trace(M, sh_g, yy, B, cs.rho64[c], cs.tra[c], bbar);
         }
     }
     // 5. q, mhat.z, mu.z; state for the next iteration (w' = L^-1 t)
@@ -567,7 +582,6 @@ __global__ void __launch_bounds__(kWideNT2, 5) k2w_update(UpdateArgs a) {
         qc[2] += cs.mu[o] * (double)z32;
         cs.z32[o] = z32;
         cs.tprev[o] = t;
-        cs.yprev[o] = xf[j];
     }
     block_sum<3>(qc, scratch);
     if (tid == 0) {

@@ -323,4 +323,208 @@ __device__ void tri_bwd(const double* __restrict__ M, int B, double* x, double* 
     }
 }
 
+
+// ---------------------------------------------------------------- streamed solves (k2w_update)
+// The per-iteration solves read the whole solve-ready factor once forward (lower part, row
+// blocks top-down) and once backward (mirrored upper part, bottom-up): 2 x 105 tiles of 32 x 32
+// fp64 at B = 425. The tile loads do not depend on the solution, only the FMAs do, so the
+// factor is streamed through a ring of S shared-memory stages by TMA (3-D map {B, B, cols} over
+// the [cols][B][wide_ld(B)] factor; rows and columns past B are zero-filled) in the exact order
+// the solves consume it, and the HBM stream runs ahead of the dependent chain by S tiles --
+// across the forward/backward boundary and the 3 x 3 algebra between them too. Thread 0
+// issues the loads (it waits on a stage's `empty` barrier, which the four warps arrive on
+// after reading the tile); no producer warp, so the 128-thread generic loops are unchanged.
+// Consumption: warp w owns tile rows 8w..8w+7, lane = tile column (conflict-free 256-byte
+// row reads); per-lane partial sums of the row block are reduced once per row block by a
+// butterfly reduce-scatter.
+constexpr int kTileD = kChB * kChB;   // doubles per factor tile
+#ifndef SMF_K2W_STAGES
+#define SMF_K2W_STAGES 3
+#endif
+constexpr int kTsS = SMF_K2W_STAGES;  // ring depth (k2w_update: five CTAs per SM at B = 425)
+
+// Stage index / phase bookkeeping is incremental (no divisions) and the issuing thread walks
+// the tile order with a cursor (no triangular decode): thread 0 is also a consumer, so every
+// cycle it spends issuing is on warp 0's path.
+struct TileStream {
+    double* ring;          // [kTsS][32][32] shared, 128-byte aligned
+    uint64_t* full;        // [kTsS] TMA completion
+    uint64_t* empty;       // [kTsS] one arrival per warp
+    const CUtensorMap* map;
+    int nblk, col;
+    int total;             // tiles in the whole sequence (forward + backward)
+    int consumed;          // every thread: tiles consumed (program order)
+    int cs, cph;           // every thread: stage and full-barrier phase of the next tile to consume
+    // thread 0 (issuer): tiles issued, stage / empty phase of the next issue, tile cursor
+    int issued, ps, pph, pI, pJ, pfwd;
+};
+
+__device__ __forceinline__ void ts_init(TileStream& ts, double* ring, uint64_t* full, uint64_t* empty,
+                                        const CUtensorMap* map, int B, int col, int npass) {
+    ts.ring = ring;
+    ts.full = full;
+    ts.empty = empty;
+    ts.map = map;
+    ts.nblk = (B + kChB - 1) / kChB;
+    ts.col = col;
+    ts.total = npass * ts.nblk * (ts.nblk + 1) / 2;
+    ts.consumed = 0;
+    ts.cs = 0;
+    ts.cph = 0;
+    ts.issued = 0;
+    ts.ps = 0;
+    ts.pph = 0;
+    ts.pI = 0;
+    ts.pJ = 0;
+    ts.pfwd = 1;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTsS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], blockDim.x >> 5);
+        }
+        fence_mbar_init();
+    }
+}
+
+// Thread 0: issue tiles up to (not including) `upto`. Order: forward row blocks I = 0.. with
+// J = 0..I (diagonal last), then backward row blocks I = nblk-1..0 with J = nblk-1..I.
+__device__ __forceinline__ void ts_issue(TileStream& ts, int upto) {
+    while (ts.issued < ts.total && ts.issued < upto) {
+        if (ts.issued >= kTsS) {
+            mbar_wait(&ts.empty[ts.ps], (uint32_t)ts.pph);   // the stage's previous tile released
+            fence_proxy_async();   // the warps' generic reads of the stage before the async refill
+        }
+        mbar_arrive_expect_tx(&ts.full[ts.ps], kTileD * 8);
+        tma_load_3d(ts.ring + (size_t)ts.ps * kTileD, ts.map, &ts.full[ts.ps], ts.pJ * kChB, ts.pI * kChB, ts.col);
+        ++ts.issued;
+        if (++ts.ps == kTsS) {
+            ts.ps = 0;
+            if (ts.issued > kTsS) ts.pph ^= 1;   // the first round of issues waits on no release
+        }
+        if (ts.pfwd) {
+            if (++ts.pJ > ts.pI) {
+                ts.pJ = 0;
+                if (++ts.pI == ts.nblk) {
+                    ts.pfwd = 0;
+                    ts.pI = ts.pJ = ts.nblk - 1;
+                }
+            }
+        } else if (--ts.pJ < ts.pI) {
+            --ts.pI;
+            ts.pJ = ts.nblk - 1;
+        }
+    }
+}
+
+__device__ __forceinline__ const double* ts_acquire(TileStream& ts) {
+    if (threadIdx.x == 0) ts_issue(ts, ts.consumed + kTsS);
+    mbar_wait(&ts.full[ts.cs], (uint32_t)ts.cph);
+    return ts.ring + (size_t)ts.cs * kTileD;
+}
+
+__device__ __forceinline__ void ts_release(TileStream& ts) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&ts.empty[ts.cs]);
+    ++ts.consumed;
+    if (++ts.cs == kTsS) {
+        ts.cs = 0;
+        ts.cph ^= 1;
+    }
+}
+
+// Thread 0 waits for every issued tile still in flight (before the ring's memory is reused or
+// the CTA exits off the streamed sequence); the caller synchronises the block afterwards.
+__device__ __forceinline__ void ts_drain(TileStream& ts) {
+    if (threadIdx.x == 0) {
+        int s = ts.cs, ph = ts.cph;
+        for (int i = ts.consumed; i < ts.issued; ++i) {
+            mbar_wait(&ts.full[s], (uint32_t)ph);
+            if (++s == kTsS) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+    }
+}
+
+// One butterfly step of the reduce-scatter: N values -> N/2, keeping the upper half if `up`.
+template <int N>
+__device__ __forceinline__ void rs_step(double* v, int o, bool up) {
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) {
+        const double send = up ? v[k] : v[k + N / 2];
+        const double keep = up ? v[k + N / 2] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+}
+
+// Sum each of V (8, 16 or 32) per-lane values over the warp; lane l ends with the total of value
+// l / (32 / V) (every lane of its group of 32 / V lanes holds it).
+template <int V>
+__device__ __forceinline__ double reduce_scatter(double (&v)[V]) {
+    static_assert(V == 8 || V == 16 || V == 32, "reduce_scatter: V in {8, 16, 32}");
+    const int lane = threadIdx.x & 31;
+    int o = 16;
+    if constexpr (V >= 32) { rs_step<32>(v, o, lane & o); o >>= 1; }
+    if constexpr (V >= 16) { rs_step<16>(v, o, lane & o); o >>= 1; }
+    rs_step<8>(v, o, lane & o); o >>= 1;
+    rs_step<4>(v, o, lane & o); o >>= 1;
+    rs_step<2>(v, o, lane & o); o >>= 1;
+    for (; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    return v[0];
+}
+
+// Streamed L x = b (FWD) or L^T x = b (!FWD) in place for NR right-hand sides x [NR][B]
+// (shared); yv [NR][32] shared. 128 threads. Consumes the next nblk (nblk + 1) / 2 tiles.
+template <int NR, bool FWD>
+__device__ __forceinline__ void tri_stream(TileStream& ts, int B, double* x, double* yv) {
+    constexpr int V = 8 * NR;
+    const int tid = threadIdx.x, lane = tid & 31, r0 = (tid >> 5) * 8;
+    const int nblk = ts.nblk;
+    const int idx = lane / (32 / V), ri = r0 + idx / NR, qi = idx % NR;
+    const bool writer = (lane & (32 / V - 1)) == 0;
+    for (int step = 0; step < nblk; ++step) {
+        const int I = FWD ? step : nblk - 1 - step;
+        const int nb = min(kChB, B - I * kChB);
+        double acc[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] = 0.0;
+        const int nJ = FWD ? I : nblk - 1 - I;   // off-diagonal tiles of the row block
+        for (int jj = 0; jj < nJ; ++jj) {
+            const int J = FWD ? jj : nblk - 1 - jj;
+            const int cJ = J * kChB + lane;
+            double xv[NR];
+#pragma unroll
+            for (int q = 0; q < NR; ++q) xv[q] = cJ < B ? x[q * B + cJ] : 0.0;
+            const double* T = ts_acquire(ts);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double l = T[(r0 + i) * kChB + lane];
+#pragma unroll
+                for (int q = 0; q < NR; ++q) acc[i * NR + q] = fma(l, xv[q], acc[i * NR + q]);
+            }
+            ts_release(ts);
+        }
+        double red = reduce_scatter<V>(acc);
+        if (writer && ri < nb) yv[qi * 32 + ri] = x[qi * B + I * kChB + ri] - red;
+        __syncthreads();
+        // x_I = L_II^-1 y (lower part incl. the diagonal) or L_II^-T y (upper part)
+        double yl[NR];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) yl[q] = lane < nb ? yv[q * 32 + lane] : 0.0;
+        const double* T = ts_acquire(ts);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int r = r0 + i;
+            const double l = (FWD ? lane <= r : lane >= r) ? T[r * kChB + lane] : 0.0;
+#pragma unroll
+            for (int q = 0; q < NR; ++q) acc[i * NR + q] = l * yl[q];
+        }
+        ts_release(ts);
+        red = reduce_scatter<V>(acc);
+        if (writer && ri < nb) x[qi * B + I * kChB + ri] = red;
+        __syncthreads();
+    }
+}
+
 }  // namespace smf
