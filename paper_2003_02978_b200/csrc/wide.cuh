@@ -619,6 +619,29 @@ __host__ inline size_t k3w_smem(int B) {
     return (kWideS3 * k3w_tile_floats(B) + 2 * (size_t)(J > 0 ? 32 * J : B)) * 4 + 16;
 }
 
+// Warp reduce-scatter of P (1, 2 or 4) fp32 sums: lane l returns the full sum of value
+// l / (32 / P). P - 1 + 5 - log2(P) shuffles instead of 5 P.
+template <int P>
+__device__ __forceinline__ float warp_rs_f(const float (&v)[P]) {
+    const int lane = threadIdx.x & 31;
+    float x0 = v[0], x1 = P > 1 ? v[P > 1 ? 1 : 0] : 0.f;
+    int o = 16;
+    if constexpr (P == 4) {   // 4 -> 2 values (lanes with bit 4 keep values 2, 3)
+        const bool up = lane & 16;
+        const float s0 = up ? v[0] : v[2], s1 = up ? v[1] : v[3];
+        x0 = (up ? v[2] : v[0]) + __shfl_xor_sync(0xffffffffu, s0, 16);
+        x1 = (up ? v[3] : v[1]) + __shfl_xor_sync(0xffffffffu, s1, 16);
+        o = 8;
+    }
+    if constexpr (P >= 2) {   // 2 -> 1 value
+        const bool up = lane & o;
+        x0 = (up ? x1 : x0) + __shfl_xor_sync(0xffffffffu, up ? x0 : x1, o);
+        o >>= 1;
+    }
+    for (; o >= 1; o >>= 1) x0 += __shfl_xor_sync(0xffffffffu, x0, o);
+    return x0;
+}
+
 // J = elements per lane of a pixel row (B <= 32 J). A warp processes PB pixels at once
 // (their dot products interleaved for ILP): lane l holds bands l + 32 j of each row in
 // registers from the albedo dot through the projection to the sum of beta L' (the
@@ -661,15 +684,17 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
     fence_proxy_async();
     __syncthreads();
 
-    auto tile_src = [&](long long gt, int& rows) -> const float* {
-        const int c = (int)(gt / a.tpc), tt = (int)(gt - (long long)c * a.tpc);
-        const int p0 = tt * kWideT3;
+    // tile addresses from cursors (column, tile-in-column): no 64-bit divisions per tile
+    auto tile_src = [&](const TileCursor& tc, int& rows) -> const float* {
+        const int p0 = tc.tt * kWideT3;
         rows = min(kWideT3, a.N - p0);
-        return L + ((size_t)c * a.N + p0) * B;
+        return L + ((size_t)tc.c * a.N + p0) * B;
     };
+    TileCursor lcur(tb, a.tpc);   // next tile to load
     auto load_tile = [&](int i) {
         int rows;
-        const float* src = tile_src(tb + i, rows);
+        const float* src = tile_src(lcur, rows);
+        lcur.next();
         float* dst = buf0 + (i % kWideS3) * TF + wide_tile_shift(src);
         if (a.bulk) {   // one TMA bulk copy (source 16-byte aligned, 16-byte multiple)
             if (tid == 0) {
@@ -786,7 +811,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             cp_async_wait_ring();   // this thread's copies of tile i have landed
         __syncthreads();        // ... and everyone's; sh_aprev visible
         int rr_;
-        const float* T = buf0 + (i % kWideS3) * TF + wide_tile_shift(tile_src(tb + i, rr_));
+        const float* T = buf0 + (i % kWideS3) * TF + wide_tile_shift(tile_src(ccur, rr_));
         for (int base = wid * PB; base < rows; base += NW * PB) {
             float v[PB][J], r[PB], dz[PB], r2[PB], dz2[PB];   // two partial sums per dot (ILP)
             int bad[PB];
@@ -813,10 +838,11 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
 #pragma unroll
                 for (int pb = 0; pb < PB; ++pb) bad[pb] = __any_sync(0xffffffffu, bad[pb]);
             }
+            // the PB dots reduced together (reduce-scatter: lane l ends with the dot of pixel
+            // l / (32 / PB)), then gathered back to every lane for the centring
+            const float rmine = warp_rs_f<PB>(r);
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-                for (int pb = 0; pb < PB; ++pb) r[pb] += __shfl_xor_sync(0xffffffffu, r[pb], off);
+            for (int pb = 0; pb < PB; ++pb) r[pb] = __shfl_sync(0xffffffffu, rmine, pb * (32 / PB));
             float scv[PB];
 #pragma unroll
             for (int pb = 0; pb < PB; ++pb) {
@@ -831,26 +857,18 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
                 }
                 dz[pb] += dz2[pb];
             }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-                for (int pb = 0; pb < PB; ++pb) dz[pb] += __shfl_xor_sync(0xffffffffu, dz[pb], off);
-            // pixel tails in parallel: lane l evaluates pixel l % PB (the PB tails share one
-            // instruction stream), then beta is broadcast for the sums
-            const int myp = lane % PB;
-            float r0 = r[0], sc = scv[0], dzm = dz[0];
+            // pixel tails in parallel: lane l evaluates pixel l / (32 / PB) (the PB tails share
+            // one instruction stream; lanes 0, 32 / PB, ... store), then beta is broadcast
+            const float dzm = warp_rs_f<PB>(dz);
+            const int myp = lane / (32 / PB);
+            const float r0 = rmine, sc = rmine * mmf;
             int badm = bad[0];
 #pragma unroll
             for (int pb = 1; pb < PB; ++pb)
-                if (myp == pb) {
-                    r0 = r[pb];
-                    sc = scv[pb];
-                    dzm = dz[pb];
-                    badm = bad[pb];
-                }
+                if (myp == pb) badm = bad[pb];
             const int ppm = base + myp;
             float beta = 0.f;
-            const bool mine = lane < PB && ppm < rows;
+            const bool mine = (lane & (32 / PB - 1)) == 0 && ppm < rows;
             if (ppm < rows) {
                 const size_t pix = (size_t)c * a.N + p0 + ppm;
                 if (cst != COL_OK || badm) {   // failed column or nodata pixel
@@ -888,7 +906,7 @@ __global__ void __launch_bounds__(kWideNT3, 4) k3w_sweep(SweepArgs a, const floa
             if (accum) {
 #pragma unroll
                 for (int pb = 0; pb < PB; ++pb) {
-                    const float bp = __shfl_sync(0xffffffffu, beta, pb);   // 0 for skipped pixels
+                    const float bp = __shfl_sync(0xffffffffu, beta, pb * (32 / PB));   // 0 for skipped pixels
                     if (base + pb < rows && bp != 0.f) {   // warp-uniform
 #pragma unroll
                         for (int j = 0; j < J; ++j) acc[j] = fmaf(bp, v[pb][j], acc[j]);
