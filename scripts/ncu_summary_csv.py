@@ -70,7 +70,8 @@ def main(src, out):
         for name, (n, t) in agg.items():
             lines.append(f"{name:<40} {n:>8} {t / 1e3:>12.1f} {t / n / 1e3:>10.2f} {t / tot:>7.3f}")
         open(os.path.join(out, f"launches_{cfg}.txt"), "w").write("\n".join(lines) + "\n")
-    tj = {}
+    tjp = os.path.join(os.path.dirname(out.rstrip("/")), "traffic.json")
+    tj = json.load(open(tjp)) if os.path.exists(tjp) else {}   # merge: a partial capture set keeps the rest
     if "fl_k3" in traffic:
         tj["flightline"] = {"k3_sweep": traffic["fl_k3"], "source": "profiles/r02/ncu_fl_k3.txt"}
     if "st_k3w" in traffic:
