@@ -30,55 +30,73 @@ constexpr int kChB = 32;         // block width of the factorisation and the sol
 __host__ __device__ inline int wide_ld(int B) { return (B + 1) & ~1; }
 constexpr int kChD = kChB + 1;   // padded row stride of the shared diagonal block
 
-// Factor and invert the diagonal block at k0 (nb <= 32 rows) by the calling warp: stage
-// the lower part of A into D, factor it in registers (lane l holds row l; column j of L is
-// read across lanes with shuffles), invert it into Dinv (lane c computes column c).
-// Returns false (warp-uniformly) on a pivot <= tol or non-finite.
-__device__ bool chol_diag_warp(const double* A, int B, int k0, int nb, double tol, double* D, double* Dinv) {
+// Factor and invert the diagonal block at k0 (nb <= 32 rows) by the calling warp. Lane l holds
+// row l in registers; the column loop is rolled and the row registers rotate one place per
+// step, so the current column is always r[0] and every register index is a compile-time
+// constant (the inner 31-wide updates are unrolled: independent FMAs fed by shuffles). The
+// fully unrolled 32 x 32 version (~20 K straight-line instructions per call, on the
+// look-ahead's critical path once per panel step) was instruction-fetch bound inside the
+// kernel (`scripts/micro/diag_bench.cu` times one call in isolation: 13.7 us now). The pivot
+// uses the hardware reciprocal square root with Newton steps (the IEEE sqrt and division are
+// long software sequences on this serial chain). The inverse (lane c computes column c of
+// L_KK^-1, right-looking with the reciprocal pivots) rotates the same way. Writes L to D and
+// L^-1 to Dinv (lower triangles, zeros elsewhere). Returns false (warp-uniformly) on a pivot
+// <= tol or non-finite.
+__device__ __forceinline__ bool chol_diag_warp(const double* A, int B, int k0, int nb, double tol, double* D,
+                                            double* Dinv) {
     const int lane = threadIdx.x & 31;
+    const double* Ar = A + (size_t)(k0 + (lane < nb ? lane : 0)) * wide_ld(B) + k0;
     double r[kChB];
 #pragma unroll
-    for (int m = 0; m < kChB; ++m) r[m] = (lane < nb && m <= lane) ? A[(size_t)(k0 + lane) * wide_ld(B) + k0 + m] : 0.0;
+    for (int m = 0; m < kChB; ++m) r[m] = (lane < nb && m <= lane) ? Ar[m] : 0.0;
     bool ok = true;
-#pragma unroll
-    for (int j = 0; j < kChB; ++j) {
-        if (j < nb) {
-            const double d = __shfl_sync(0xffffffffu, r[j], j);
-            if (!(d > tol) || !isfinite(d)) ok = false;   // warp-uniform
-            const double g = sqrt(fmax(d, 0.0));
-            const double ginv = 1.0 / g;
-            if (lane == j) r[j] = g;
-            else if (lane > j) r[j] *= ginv;   // L_lj
-            const double lj = r[j];
-#pragma unroll
-            for (int m = j + 1; m < kChB; ++m) {
-                const double lmj = __shfl_sync(0xffffffffu, r[j], m);   // L_mj
-                if (lane >= m) r[m] = fma(-lj, lmj, r[m]);
-            }
+    double rdl = 0.0;   // lane j: 1 / L_jj
+#pragma unroll 1
+    for (int j = 0; j < nb; ++j) {
+        const double d = __shfl_sync(0xffffffffu, r[0], j);
+        if (!(d > tol) || !isfinite(d)) ok = false;   // warp-uniform (the factor is then discarded)
+        // 1/sqrt(d) by the hardware reciprocal-square-root seed and Newton steps, g = d / sqrt(d):
+        // the IEEE sqrt and division are software sequences of ~1000 cycles each on this
+        // critical path (one pivot after another); ~1 ulp apart from them
+        const double ginv = rsqrt(d);
+        const double g = d * ginv;
+        if (lane == j) {
+            r[0] = g;
+            rdl = ginv;   // reciprocal pivot for the inverse below
         }
-    }
+        else if (lane > j) r[0] *= ginv;   // L_lj
+        const double lj = r[0];
 #pragma unroll
-    for (int m = 0; m < kChB; ++m) D[lane * kChD + m] = r[m];
+        for (int m = 1; m < kChB; ++m) {   // original column j + m
+            const double lmj = __shfl_sync(0xffffffffu, r[0], (j + m) & 31);
+            if (lane >= j + m) r[m] = fma(-lj, lmj, r[m]);
+        }
+        D[lane * kChD + j] = r[0];   // column j of row `lane` is final
+#pragma unroll
+        for (int m = 0; m < kChB - 1; ++m) r[m] = r[m + 1];
+        r[kChB - 1] = 0.0;
+    }
+    for (int j = nb; j < kChB; ++j) D[lane * kChD + j] = 0.0;
     __syncwarp();
     if (ok) {
-        // column `lane` of L_KK^-1 by right-looking substitution: once x_k is final, every
-        // later x_i takes its update at once (independent FMAs; the dependent chain is 32
-        // steps, not the 500 of a dot product per entry)
-        Dinv[lane * kChD + lane] = lane < nb ? 1.0 / D[lane * kChD + lane] : 0.0;   // reciprocal pivots
-        __syncwarp();
-        double x[kChB];
+        double x[kChB];   // x[i] = row k + i of column `lane` at step k
 #pragma unroll
-        for (int i = 0; i < kChB; ++i) x[i] = i == lane ? 1.0 : 0.0;
+        for (int i = 0; i < kChB; ++i) x[i] = (i == lane && i < nb) ? 1.0 : 0.0;
+#pragma unroll 1
+        for (int k = 0; k < nb; ++k) {
+            const double xk = x[0] * __shfl_sync(0xffffffffu, rdl, k);
+            Dinv[k * kChD + lane] = xk;
+            const double* Dk = D + k;   // column k of L, rows k + i
 #pragma unroll
-        for (int k = 0; k < kChB; ++k) {
-            const double xk = x[k] * Dinv[k * kChD + k];
-            x[k] = xk;
+            for (int i = 1; i < kChB; ++i) {
+                const double l = k + i < nb ? Dk[(k + i) * kChD] : 0.0;
+                x[i] = fma(-l, xk, x[i]);
+            }
 #pragma unroll
-            for (int i = k + 1; i < kChB; ++i) x[i] = fma(-D[i * kChD + k], xk, x[i]);
+            for (int i = 0; i < kChB - 1; ++i) x[i] = x[i + 1];
+            x[kChB - 1] = 0.0;
         }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < kChB; ++i) Dinv[i * kChD + lane] = i < nb ? x[i] : 0.0;
+        for (int i = nb; i < kChB; ++i) Dinv[i * kChD + lane] = 0.0;
     }
     __syncwarp();
     return ok;
@@ -153,6 +171,7 @@ __device__ __forceinline__ void tri_decode(int e, int& I, int& J) {
 // the next diagonal block while the other warps apply the rest of the trailing update.
 // D, Dinv: shared [kChB][kChD]; Cp: shared [B][kChB] (16-byte aligned, swizzled pairs); flag:
 // shared int. Returns false (uniformly) on a non-positive or non-finite pivot (<= tol).
+
 __device__ bool wide_cholesky(double* A, int B, double tol, double* D, double* Dinv, double* Cp, int* flag) {
     const int tid = threadIdx.x, nt = blockDim.x, wid = tid >> 5;
     if (tid == 0) *flag = 0;
