@@ -153,7 +153,7 @@ constexpr int kI8QTiles = 4;   // 128-pixel tiles per k1w_quant block (amortises
 // gamma = 1; rows >= R: 0). A non-finite v becomes 0 -- which also zeroes nodata pixels
 // (sigma = NaN) and the pixels past N (sigma set to NaN here); non-finite data was flagged by
 // k1w_scan (+inf row maximum) and turns the partial into NaN in the SYRK epilogue.
-__global__ void __launch_bounds__(256) k1w_quant(I8QuantArgs a) {
+__global__ void __launch_bounds__(256, 5) k1w_quant(I8QuantArgs a) {
     extern __shared__ uint32_t qsm[];   // [4][64 rows][33 words]: 4 pixels per word, padded
     const int rb = blockIdx.y, c = blockIdx.z, tid = threadIdx.x;
     const int B = a.B, R = a.R;
@@ -217,16 +217,20 @@ __global__ void __launch_bounds__(256) k1w_quant(I8QuantArgs a) {
                 }
             }
         __syncthreads();
-        // write out: warp = 8 (slice, row) pairs per pass, lane = word (128 B per row segment)
+        // write out: warp = 8 rows per pass, lane = word (128 B per row segment); 32-bit word
+        // offsets from a per-slice base (a column's slices are 4 R Np bytes), no per-store
+        // 64-bit address arithmetic
         const int w = tid & 31, pw_lim = min(kI8QTile, a.Np - pbase) / 4;   // Np is a multiple of 16
-        if (w < pw_lim)
-            for (int sr = tid >> 5; sr < kI8S * kI8QRows; sr += 8) {
-                const int s = sr / kI8QRows, rr = sr - s * kI8QRows;
-                if (rr >= nrows) continue;
-                uint32_t* dst =
-                    reinterpret_cast<uint32_t*>(a.slices + (((size_t)c * kI8S + s) * R + rbase + rr) * a.Np + pbase);
-                dst[w] = qsm[sr * 33 + w];
+        if (w < pw_lim) {
+            const int wpr = a.Np >> 2;   // words per slice row
+            const uint32_t* qs = qsm + w;
+#pragma unroll
+            for (int sl = 0; sl < kI8S; ++sl) {
+                uint32_t* dst = reinterpret_cast<uint32_t*>(a.slices + (((size_t)c * kI8S + sl) * R + rbase) * a.Np +
+                                                            pbase) + w;
+                for (int rr = tid >> 5; rr < nrows; rr += 8) dst[rr * wpr] = qs[(sl * kI8QRows + rr) * 33];
             }
+        }
     }
 }
 

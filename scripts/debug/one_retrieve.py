@@ -1,8 +1,8 @@
 """One warm-up retrieval plus one retrieval of a BASELINE config (for ncu captures: the second
 retrieval's launches are the ones to profile)."""
-import sys
+import os, sys
 import torch
-sys.path.insert(0, ".")
+sys.path.insert(0, os.environ.get("VARIANT_ROOT", "."))
 from paper_2003_02978_b200 import synth, smf
 
 name = sys.argv[1] if len(sys.argv) > 1 else "flightline"
