@@ -176,17 +176,30 @@ __global__ void __launch_bounds__(256, 5) k1w_quant(I8QuantArgs a) {
             sh_sig[p] = gp < a.N ? a.sigma[(size_t)c * a.N + gp] : __int_as_float(0x7fc00000);
         }
         const int nvalid = a.N - pbase;   // pixels of this tile that exist (may exceed 128)
-        const float* Lr = a.L + ((size_t)c * a.N + pbase) * B + gr;
+        // block-uniform 64-bit base + 32-bit per-thread offsets (p B + gr < 2^31): one integer
+        // add per load instead of a 64-bit multiply-add chain
+        const float* Lt = a.L + ((size_t)c * a.N + pbase) * B;
+        const uint32_t o0 = (uint32_t)(4 * q * B + gr), o16 = (uint32_t)(16 * B), oB = (uint32_t)B;
         float lv[2][4][4];   // all 32 of this thread's radiances in flight at once
+        if (band && nvalid >= kI8QTile) {   // full tile: no per-load bounds
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int p = 4 * (q + 4 * (4 * h + u)) + k;
-                    lv[h][u][k] = (band && p < nvalid) ? __ldg(Lr + (size_t)p * B) : 0.f;
-                }
+                    for (int k = 0; k < 4; ++k) lv[h][u][k] = __ldg(Lt + (o0 + (uint32_t)(4 * h + u) * o16 + k * oB));
+        } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int p = 4 * (q + 4 * (4 * h + u)) + k;
+                        lv[h][u][k] =
+                            (band && p < nvalid) ? __ldg(Lt + (o0 + (uint32_t)(4 * h + u) * o16 + k * oB)) : 0.f;
+                    }
+        }
         __syncthreads();
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -213,7 +226,10 @@ __global__ void __launch_bounds__(256, 5) k1w_quant(I8QuantArgs a) {
                 for (int d = 0; d < kI8S; ++d) {
                     const uint32_t lo = __byte_perm(dgk[0][d], dgk[1][d], 0x0040);
                     const uint32_t hi = __byte_perm(dgk[2][d], dgk[3][d], 0x0040);
-                    qsm[(d * kI8QRows + r) * 33 + w] = __vsub4(__byte_perm(lo, hi, 0x5410), 0x40404040u);
+                    // per byte b in [0, 127]: b - 64 as int8 = b ^ 0x40 ^ ((~b & 0x40) << 1) (no
+                    // borrows between bytes; __vsub4 is a multi-instruction sequence)
+                    const uint32_t wb = __byte_perm(lo, hi, 0x5410);
+                    qsm[(d * kI8QRows + r) * 33 + w] = wb ^ 0x40404040u ^ ((~wb & 0x40404040u) << 1);
                 }
             }
         __syncthreads();
@@ -222,13 +238,23 @@ __global__ void __launch_bounds__(256, 5) k1w_quant(I8QuantArgs a) {
         // 64-bit address arithmetic
         const int w = tid & 31, pw_lim = min(kI8QTile, a.Np - pbase) / 4;   // Np is a multiple of 16
         if (w < pw_lim) {
-            const int wpr = a.Np >> 2;   // words per slice row
+            const uint32_t wpr = (uint32_t)a.Np >> 2;   // words per slice row
             const uint32_t* qs = qsm + w;
+            const int r0 = tid >> 5;
 #pragma unroll
             for (int sl = 0; sl < kI8S; ++sl) {
+                // block-uniform base, 32-bit word offsets (a column's slices are 4 R Np bytes)
                 uint32_t* dst = reinterpret_cast<uint32_t*>(a.slices + (((size_t)c * kI8S + sl) * R + rbase) * a.Np +
-                                                            pbase) + w;
-                for (int rr = tid >> 5; rr < nrows; rr += 8) dst[rr * wpr] = qs[(sl * kI8QRows + rr) * 33];
+                                                            pbase);
+                if (nrows == kI8QRows) {
+#pragma unroll
+                    for (int i = 0; i < kI8QRows / 8; ++i) {
+                        const int rr = r0 + 8 * i;
+                        dst[(uint32_t)rr * wpr + w] = qs[(sl * kI8QRows + rr) * 33];
+                    }
+                } else {
+                    for (int rr = r0; rr < nrows; rr += 8) dst[(uint32_t)rr * wpr + w] = qs[(sl * kI8QRows + rr) * 33];
+                }
             }
         }
     }
