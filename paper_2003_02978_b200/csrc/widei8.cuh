@@ -72,7 +72,7 @@ __host__ inline int k1w_scan_j(int B) { return B <= 64 ? 2 : B <= 128 ? 4 : B <=
 // maxima of v = L - sigma c kept per lane across the warp's pixels, combined across warps in
 // shared memory and merged into vmax with one atomicMax per (block, row)
 template <int J>
-__global__ void __launch_bounds__(256, 3) k1w_scan(I8ScanArgs a) {
+__global__ void __launch_bounds__(256, 4) k1w_scan(I8ScanArgs a) {
     const int c = blockIdx.y, p0 = blockIdx.x * kI8ScanPix, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int np = min(kI8ScanPix, a.N - p0), B = a.B;
     __shared__ float red[8][kI8ScanJ * 32 + 2];
