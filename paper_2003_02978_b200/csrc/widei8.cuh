@@ -153,7 +153,7 @@ constexpr int kI8QTiles = 4;   // 128-pixel tiles per k1w_quant block (amortises
 // gamma = 1; rows >= R: 0). A non-finite v becomes 0 -- which also zeroes nodata pixels
 // (sigma = NaN) and the pixels past N (sigma set to NaN here); non-finite data was flagged by
 // k1w_scan (+inf row maximum) and turns the partial into NaN in the SYRK epilogue.
-__global__ void __launch_bounds__(256, 5) k1w_quant(I8QuantArgs a) {
+__global__ void __launch_bounds__(256, 4) k1w_quant(I8QuantArgs a) {
     extern __shared__ uint32_t qsm[];   // [4][64 rows][33 words]: 4 pixels per word, padded
     const int rb = blockIdx.y, c = blockIdx.z, tid = threadIdx.x;
     const int B = a.B, R = a.R;
