@@ -857,7 +857,7 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         ia.use_albedo = ctx->use_albedo;
         ia.stats_only = stats_only;
         ia.energy = ctx->energy;
-        ia.sym = p.widei8 ? 1 : 0;
+        ia.sym = 0;   // diagonal 128-blocks are (P + P^T)/2 for every statistics kernel (int8: 7-MMA diagonal pairs)
         ia.ridge_rel = ctx->ridge;
         e = cudaFuncSetAttribute(k2w_init, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem2);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init smem attribute");

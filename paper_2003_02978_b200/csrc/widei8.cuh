@@ -21,7 +21,7 @@
 //             int8 slice cube [cols][4][R = B + 2][Np] (transposed through shared memory)
 //  k1w_syrk_i8  persistent; a work item = (column, 128 x 128 row-block pair m >= n); TMA
 //             loads the 4 (diagonal) or 8 slice tiles of 128 rows x 64 pixels per K tile
-//             (SWIZZLE_64B); one thread issues the 10 kind::i8 MMAs per 32-pixel K step into
+//             (SWIZZLE_64B); one thread issues the 10 (diagonal pairs: 7) kind::i8 MMAs per 32-pixel K step into
 //             four int32 TMEM accumulators (all 512 columns); 4 epilogue warps combine them in
 //             fp64 into the column's [BEp][BEp] partial that k2w_init consumes.
 #pragma once
@@ -381,12 +381,17 @@ __global__ void __launch_bounds__(kI8NT, 1)
                             }
                             const uint32_t acc = (kt == kt0 && ks == 0) ? 0u : 1u;
                             // accumulator j (TMEM columns 128 j) collects the digit products of
-                            // weight 2^(42 - 7 j): k + l = j (0-based digit indices)
+                            // weight 2^(42 - 7 j): k + l = j (0-based digit indices). A diagonal
+                            // block pair (m = n) needs only k <= l for j = 1, 3 (the k > l products
+                            // are transposes; the epilogue doubles those accumulators and k2w_init
+                            // symmetrises the block): 7 MMAs instead of 10. j = 2 mixes the
+                            // cross product with the square D1 D1^T, so it keeps all three.
 #pragma unroll
                             for (int j = 0; j < kI8S; ++j)
 #pragma unroll
                                 for (int k = 0; k <= j; ++k)
-                                    mma_i8(tmem + 128 * j, ad[k], bd[j - k], idesc, k == 0 ? acc : 1u);
+                                    if (!(diag && (j & 1) && k > j - k))
+                                        mma_i8(tmem + 128 * j, ad[k], bd[j - k], idesc, k == 0 ? acc : 1u);
                         }
                         mma_commit(&empty[s]);
                     }
@@ -409,6 +414,8 @@ __global__ void __launch_bounds__(kI8NT, 1)
             const bool badi = !(__uint_as_float(vbi) <= 3.402823466e38f);
             const int ei = i8_exponent(vbi);
             double* prow = a.part + ((size_t)c * a.BEp + gi) * a.BEp + (size_t)n * kI8Blk;
+            // diagonal pairs carry the odd-j cross products once (see the MMA issuer): doubled here
+            const double w1 = m == n ? 32768.0 : 16384.0, w3 = m == n ? 2.0 : 1.0;
             for (int kt0 = 0; kt0 < ntile; kt0 += kI8MaxRun) {
                 mbar_wait(&acc_full, runs & 1);
                 tc_fence_after();
@@ -426,8 +433,8 @@ __global__ void __launch_bounds__(kI8NT, 1)
                         const bool bad = badi || !(__uint_as_float(vbj) <= 3.402823466e38f);
                         // sum_i q_a q_b = 2^42 x0 + 2^35 x1 + 2^28 x2 + 2^21 x3 (each term exact in
                         // fp64; the sum rounds once per term at 2^-53)
-                        const double sumq = (((double)x[0][k] * 2097152.0 + (double)x[1][k] * 16384.0) +
-                                             (double)x[2][k] * 128.0) + (double)x[3][k];
+                        const double sumq = (((double)x[0][k] * 2097152.0 + (double)x[1][k] * w1) +
+                                             (double)x[2][k] * 128.0) + (double)x[3][k] * w3;
                         double v = bad ? __longlong_as_double(0x7ff8000000000000ULL)
                                        : ldexp(sumq, ei + i8_exponent(vbj) - 54 + 21);
                         if (kt0 > 0) v += prow[j0 + k];
