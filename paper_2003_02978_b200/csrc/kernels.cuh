@@ -783,10 +783,11 @@ struct PilotArgs {
     float nodata;
     unsigned* vmax;   // wide int8 statistics: per-row maxima [cols][BEq], zeroed here (or NULL)
     int BEq;
+    int c0 = 0;       // first column of this launch (grid.x columns from c0)
 };
 
 __global__ void k0_pilot(PilotArgs a) {
-    const int c = blockIdx.x, tid = threadIdx.x;
+    const int c = a.c0 + blockIdx.x, tid = threadIdx.x;
     if (a.vmax)
         for (int b = tid; b < a.BEq; b += blockDim.x) a.vmax[(size_t)c * a.BEq + b] = 0u;
     __shared__ double cc;

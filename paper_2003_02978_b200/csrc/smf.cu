@@ -70,6 +70,10 @@ struct smf_ctx {
         }
     } gkey = {};
     int glaunches = 0;
+    // wide path: the last partial wave of k2w_init runs on this stream beside the other
+    // columns' statistics (retrieve_eager); created on first use
+    cudaStream_t aux = nullptr;
+    cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
 };
 
 namespace {
@@ -668,9 +672,31 @@ struct GroupLayout {
     }
 };
 
+// Columns of the wide int8 path whose k2w_init is split off the main launch (0: no split): the
+// partial last wave, when it is at most half a wave. SMF_TAIL_SPLIT=0 disables it (A/B).
+int wide_tail_mode() {
+    static const int mode = [] {
+        const char* e = std::getenv("SMF_TAIL_SPLIT");
+        return e ? std::atoi(e) : 1;
+    }();
+    return mode;
+}
+
+int wide_tail_cols(const smf_ctx* ctx, const Plan& p) {
+    const int on = wide_tail_mode();
+    if (!on || !p.wide || !p.widei8 || ctx->prof || p.cols <= ctx->sm_count) return 0;
+    const int tail = p.cols % ctx->sm_count;
+    return tail <= ctx->sm_count / 2 ? tail : 0;
+}
+
 // K0 pilot + K1 stats + K2 init (shared by retrieve and initial_statistics)
+// Wide int8 path only: columns [c0, c0 + nc) of the plan (nc < 0: all), and k2w_init on st_init
+// (ordered behind this range's statistics by ctx->aux_fork) instead of st.
 smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned char* ws, cudaStream_t st,
-                        double* mean_out, double* cov_out, int stats_only, int& launches) {
+                        double* mean_out, double* cov_out, int stats_only, int& launches, int c0 = 0, int nc = -1,
+                        cudaStream_t st_init = nullptr) {
+    if (nc < 0) nc = p.cols;
+    const bool fork = st_init != nullptr && st_init != st;
     CUtensorMap mm, tm;
     if (!p.wide) {
         CUresult cr = make_maps(rad, p.cols, p.N, p.B, &mm, &tm, p.T1);
@@ -690,9 +716,10 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
     pa.nodata = ctx->nodata;
     pa.vmax = p.widei8 ? (unsigned*)(ws + p.o_vmax) : nullptr;
     pa.BEq = p.BEq8;
+    pa.c0 = c0;
     {
         ProfScope ps(ctx, st, SMF_KERNEL_STATS);
-        k0_pilot<<<p.cols, 128, 0, st>>>(pa);
+        k0_pilot<<<nc, 128, 0, st>>>(pa);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k0_pilot launch");
@@ -712,9 +739,10 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         sc.BEq = p.BEq8;
         sc.mask = ctx->mask;
         sc.nodata = ctx->nodata;
+        sc.c0 = c0;
         {
             ProfScope ps(ctx, st, SMF_KERNEL_STATS);
-            const dim3 grid((p.N + kI8ScanPix - 1) / kI8ScanPix, p.cols);
+            const dim3 grid((p.N + kI8ScanPix - 1) / kI8ScanPix, nc);
             switch (k1w_scan_j(p.B)) {
                 case 2: k1w_scan<2><<<grid, 256, 0, st>>>(sc); break;
                 case 4: k1w_scan<4><<<grid, 256, 0, st>>>(sc); break;
@@ -739,11 +767,12 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         qa.Np = p.Np8;
         qa.BEq = p.BEq8;
         qa.mask = ctx->mask;
+        qa.c0 = c0;
         e = cudaFuncSetAttribute(k1w_quant, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1w_quant_smem());
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_quant smem attribute");
         {
             ProfScope ps(ctx, st, SMF_KERNEL_STATS);
-            k1w_quant<<<dim3((p.Np8 + kI8QTile * kI8QTiles - 1) / (kI8QTile * kI8QTiles), (p.R8 + kI8QRows - 1) / kI8QRows, p.cols), 256,
+            k1w_quant<<<dim3((p.Np8 + kI8QTile * kI8QTiles - 1) / (kI8QTile * kI8QTiles), (p.R8 + kI8QRows - 1) / kI8QRows, nc), 256,
                         k1w_quant_smem(), st>>>(qa);
         }
         e = cudaGetLastError();
@@ -774,7 +803,8 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         ya.BEp = p.NBLKw * 128;
         ya.NBLK = p.NBLKw;
         ya.npairs = p.NBLKw * (p.NBLKw + 1) / 2;
-        ya.nitems = p.cols * ya.npairs;
+        ya.nitems = nc * ya.npairs;
+        ya.c0 = c0;
         e = cudaFuncSetAttribute(k1w_syrk_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1w_i8_smem());
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k1w_syrk_i8 smem attribute");
         {
@@ -859,14 +889,22 @@ smf_status launch_stats(smf_ctx* ctx, const Plan& p, const float* rad, unsigned 
         ia.energy = ctx->energy;
         ia.sym = 0;   // diagonal 128-blocks are (P + P^T)/2 for every statistics kernel (int8: 7-MMA diagonal pairs)
         ia.ridge_rel = ctx->ridge;
+        ia.c0 = c0;
+        cudaStream_t si = st;
+        if (fork) {   // this range's k2w_init on st_init, behind its statistics
+            e = cudaEventRecord(ctx->aux_fork, st);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(st_init, ctx->aux_fork, 0);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init fork");
+            si = st_init;
+        }
         e = cudaFuncSetAttribute(k2w_init, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem2);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init smem attribute");
         {
-            ProfScope ps(ctx, st, SMF_KERNEL_INIT);
+            ProfScope ps(ctx, si, SMF_KERNEL_INIT);
             // a power of two of warps (the solves share each row among blockDim / 32 threads)
             int nti = 32;
             while (nti < kWideNTI && nti < p.B) nti *= 2;
-            k2w_init<<<p.cols, nti, p.smem2, st>>>(ia);
+            k2w_init<<<nc, nti, p.smem2, si>>>(ia);
         }
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init launch");
@@ -1015,6 +1053,9 @@ void smf_destroy(smf_ctx* ctx) {
     for (auto ev : ctx->h_ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
+    if (ctx->aux_fork) cudaEventDestroy(ctx->aux_fork);
+    if (ctx->aux_join) cudaEventDestroy(ctx->aux_join);
     delete ctx;
 }
 
@@ -1296,8 +1337,43 @@ static smf_status retrieve_eager(smf_ctx* ctx, const float* radiance, int cols, 
     }
     unsigned char* ws = (unsigned char*)workspace;
     int launches = 0;
-    smf_status rc = launch_stats(ctx, p, radiance, ws, st, nullptr, nullptr, 0, launches);
-    if (rc != SMF_OK) return rc;
+    smf_status rc = SMF_OK;
+    const int tail = wide_tail_cols(ctx, p);
+    if (tail > 0) {
+        // k2w_init runs one CTA per SM and every column costs the same, so the last
+        // cols % SMs columns would hold a few SMs for a whole extra wave (598 columns on 148
+        // SMs: 6 columns, ~0.9 ms). Their statistics go first and their k2w_init runs on a
+        // second (high-priority) stream beside the other columns' statistics kernels; the
+        // partitions are independent and every kernel is per-column deterministic,
+        // so the results are bit-identical to the single-range launch order.
+        if (!ctx->aux) {
+            int lo = 0, hi = 0;
+            cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+            if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, hi);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->aux_join, cudaEventDisableTiming);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "auxiliary stream");
+        }
+        cudaError_t e = cudaSuccess;
+        if (wide_tail_mode() == 2) {   // the tail's statistics on the second stream too
+            e = cudaEventRecord(ctx->aux_fork, st);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->aux_fork, 0);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "tail fork");
+            rc = launch_stats(ctx, p, radiance, ws, ctx->aux, nullptr, nullptr, 0, launches, cols - tail, tail);
+        } else {
+            rc = launch_stats(ctx, p, radiance, ws, st, nullptr, nullptr, 0, launches, cols - tail, tail, ctx->aux);
+        }
+        if (rc != SMF_OK) return rc;
+        e = cudaEventRecord(ctx->aux_join, ctx->aux);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init join record");
+        rc = launch_stats(ctx, p, radiance, ws, st, nullptr, nullptr, 0, launches, 0, cols - tail);
+        if (rc != SMF_OK) return rc;
+        e = cudaStreamWaitEvent(st, ctx->aux_join, 0);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "k2w_init join");
+    } else {
+        rc = launch_stats(ctx, p, radiance, ws, st, nullptr, nullptr, 0, launches);
+        if (rc != SMF_OK) return rc;
+    }
     ColState cs = col_state(p, ws, ctx->s_dev, ctx);
     SweepArgs sa;
     sa.enh = enhancement;

@@ -224,6 +224,7 @@ struct WideInitArgs {
     int energy;            // the energy trace needs tr(A0^-1)
     int sym;               // the block-pair partials are exactly symmetric (int8 SYRK): no (P + P^T)/2
     double ridge_rel;
+    int c0 = 0;            // first column of this launch (grid.x columns from c0)
 };
 
 // shared: dm, srx, cv, vt, mh [B]; D, Dinv [32][33]; the panel Cp [B][32] (after the
@@ -236,7 +237,7 @@ __host__ inline size_t k2w_init_smem(int B) { return (size_t)(5 * B + 2 * kChB *
 
 __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
     extern __shared__ double w2_smem[];
-    const int B = a.B, tid = threadIdx.x, c = blockIdx.x, nt = blockDim.x;
+    const int B = a.B, tid = threadIdx.x, c = a.c0 + blockIdx.x, nt = blockDim.x;
     double* dm = w2_smem;        // [B] mean(L) - c, later mu0
     double* srx = dm + B;        // [B]
     double* cv = srx + B;        // [B] pilot c

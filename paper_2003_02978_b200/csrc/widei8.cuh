@@ -40,6 +40,9 @@ constexpr int kI8NT = 192;         // SYRK threads: TMA warp, MMA warp, 4 epilog
 constexpr int kI8MaxRun = 2048;    // K tiles per int32 run (131072 pixels: 4 digit products <= 4 * 64^2 per pixel)
 constexpr uint32_t kI8TileBytes = kI8Blk * kI8Tile;   // one slice of one block: 8 KB
 constexpr int kI8ScanPix = 128;    // pixels per k1w_scan block
+#ifndef SMF_I8_PAIRN
+#define SMF_I8_PAIRN 1             // A/B switch: 0 = one 128 x 128 digit product per MMA
+#endif
 
 __host__ __device__ inline size_t k1w_i8_smem() { return (size_t)kI8Stages * 2 * kI8S * kI8TileBytes + 1024; }
 __host__ __device__ inline size_t k1w_quant_smem() { return (size_t)kI8S * 64 * 33 * 4; }
@@ -62,6 +65,7 @@ struct I8ScanArgs {
     unsigned* vmax;        // out [cols][BEq] float bits, zeroed by k0_pilot; +inf = non-finite data
     int cols, N, B, BEq, mask;
     float nodata;
+    int c0 = 0;            // first column of this launch (grid.y columns from c0)
 };
 
 constexpr int kI8ScanJ = 20;   // bands per lane held in registers (B <= 640)
@@ -73,7 +77,7 @@ __host__ inline int k1w_scan_j(int B) { return B <= 64 ? 2 : B <= 128 ? 4 : B <=
 // shared memory and merged into vmax with one atomicMax per (block, row)
 template <int J>
 __global__ void __launch_bounds__(256, 4) k1w_scan(I8ScanArgs a) {
-    const int c = blockIdx.y, p0 = blockIdx.x * kI8ScanPix, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int c = a.c0 + blockIdx.y, p0 = blockIdx.x * kI8ScanPix, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int np = min(kI8ScanPix, a.N - p0), B = a.B;
     __shared__ float red[8][kI8ScanJ * 32 + 2];
     __shared__ float gs[kI8ScanJ * 32], cs_[kI8ScanJ * 32];
@@ -142,6 +146,7 @@ struct I8QuantArgs {
     const unsigned* vmax;
     int8_t* slices;        // out [cols][4][R][Np]
     int cols, N, B, R, Np, BEq, mask;
+    int c0 = 0;            // first column of this launch
 };
 
 constexpr int kI8QRows = 64;   // extended rows per k1w_quant block
@@ -155,7 +160,7 @@ constexpr int kI8QTiles = 4;   // 128-pixel tiles per k1w_quant block (amortises
 // k1w_scan (+inf row maximum) and turns the partial into NaN in the SYRK epilogue.
 __global__ void __launch_bounds__(256, 4) k1w_quant(I8QuantArgs a) {
     extern __shared__ uint32_t qsm[];   // [4][64 rows][33 words]: 4 pixels per word, padded
-    const int rb = blockIdx.y, c = blockIdx.z, tid = threadIdx.x;
+    const int rb = blockIdx.y, c = a.c0 + blockIdx.z, tid = threadIdx.x;
     const int B = a.B, R = a.R;
     __shared__ float sh_sig[kI8QTile];
     const int rbase = rb * kI8QRows;
@@ -292,6 +297,7 @@ struct I8SyrkArgs {
     const unsigned* vmax;   // [cols][BEq]
     double* part;           // out [cols][BEp][BEp] (lower blocks m >= n; diagonal blocks full)
     int cols, N, R, BEq, BEp, NBLK, npairs, nitems;
+    int c0 = 0;             // first column of this launch (items cover columns c0 .. c0 + nitems / npairs - 1)
 };
 
 __global__ void __launch_bounds__(kI8NT, 1)
@@ -301,11 +307,14 @@ __global__ void __launch_bounds__(kI8NT, 1)
     constexpr uint32_t STAGE = 2 * kI8S * kI8TileBytes;
     __shared__ uint64_t full[kI8Stages], empty[kI8Stages], acc_full, acc_empty;
     __shared__ uint32_t tmem_sh;
+    __shared__ double colsc[2][kI8Blk];   // epilogue: 2^e_j of the item's columns (by item parity)
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     const int ntile = (a.N + kI8Tile - 1) / kI8Tile;
     // M = N = 128, int8 x int8 -> s32, both K-major
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kI8Blk >> 3) << 17) |
                            ((uint32_t)(kI8Blk >> 4) << 24);
+    // the same with N = 256: two adjacent digit slices of the B block per instruction
+    const uint32_t idesc2 = (idesc & ~(0x3fu << 17)) | ((uint32_t)(2 * kI8Blk >> 3) << 17);
     if (tid == 0) {
         prefetch_tmap(&tm);
         for (int s = 0; s < kI8Stages; ++s) {
@@ -322,8 +331,9 @@ __global__ void __launch_bounds__(kI8NT, 1)
     tc_fence_after();
     const uint32_t tmem = tmem_sh;
     auto item_mn = [&](int it, int& c, int& m, int& n) {
-        c = it / a.npairs;
-        n = it - c * a.npairs;
+        const int cl = it / a.npairs;
+        c = a.c0 + cl;
+        n = it - cl * a.npairs;
         m = 0;
         while (n > m) {
             n -= m + 1;
@@ -384,14 +394,33 @@ __global__ void __launch_bounds__(kI8NT, 1)
                             // weight 2^(42 - 7 j): k + l = j (0-based digit indices). A diagonal
                             // block pair (m = n) needs only k <= l for j = 1, 3 (the k > l products
                             // are transposes; the epilogue doubles those accumulators and k2w_init
-                            // symmetrises the block): 7 MMAs instead of 10. j = 2 mixes the
+                            // symmetrises the block): 7 products instead of 10. j = 2 mixes the
                             // cross product with the square D1 D1^T, so it keeps all three.
+#if SMF_I8_PAIRN
+                            // Two products per instruction where they land in adjacent
+                            // accumulators: the digit slices of a block are adjacent 8 KB tiles of
+                            // the stage, so B = [D_l ; D_l+1] is one 256-row operand and
+                            // D_k [D_l ; D_l+1]^T fills accumulators k + l and k + l + 1 (N = 256)
+                            // with one read of A: 6 (diagonal pairs: 4) MMAs instead of 10 (7).
+                            mma_i8(tmem, ad[0], bd[0], idesc2, acc);             // (0,0) (0,1)
+                            mma_i8(tmem + 256, ad[0], bd[2], idesc2, acc);       // (0,2) (0,3)
+                            if (!diag) {
+                                mma_i8(tmem + 128, ad[1], bd[0], idesc2, 1u);    // (1,0) (1,1)
+                                mma_i8(tmem + 384, ad[1], bd[2], idesc, 1u);     // (1,2)
+                                mma_i8(tmem + 256, ad[2], bd[0], idesc2, 1u);    // (2,0) (2,1)
+                                mma_i8(tmem + 384, ad[3], bd[0], idesc, 1u);     // (3,0)
+                            } else {
+                                mma_i8(tmem + 256, ad[1], bd[1], idesc2, 1u);    // (1,1) (1,2)
+                                mma_i8(tmem + 256, ad[2], bd[0], idesc, 1u);     // (2,0)
+                            }
+#else
 #pragma unroll
                             for (int j = 0; j < kI8S; ++j)
 #pragma unroll
                                 for (int k = 0; k <= j; ++k)
                                     if (!(diag && (j & 1) && k > j - k))
                                         mma_i8(tmem + 128 * j, ad[k], bd[j - k], idesc, k == 0 ? acc : 1u);
+#endif
                         }
                         mma_commit(&empty[s]);
                     }
@@ -402,17 +431,32 @@ __global__ void __launch_bounds__(kI8NT, 1)
         }
     } else {
         // ===================== epilogue: TMEM int32 -> fp64 partial =====================
+        // v = sumq 2^(e_i + e_j - 33) as two exact power-of-two multiplications: the row's factor
+        // in a register, the 128 column factors of the item in shared memory (one per epilogue
+        // thread, double-buffered by item parity: one named barrier per item). A non-finite row
+        // maximum (flagged by k1w_scan) makes its factor NaN, which the products propagate. The
+        // per-element __ldg + frexpf + ldexp of the first version was ~110 instructions per
+        // element: ~a fifth of the kernel, with the tensor pipe idle (the accumulators are
+        // single-buffered: all 512 TMEM columns hold one item).
         const int q = wid & 3;                 // TMEM lane quadrant this warp may access
         const int rl = 32 * q + lane;          // row within the block
+        const double kNaN = __longlong_as_double(0x7ff8000000000000ULL);
+        auto pow2 = [](int e) { return __longlong_as_double((long long)(e + 1023) << 52); };   // -1022 <= e <= 1023
         uint32_t runs = 0;
-        for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+        int par = 0;
+        for (int it = blockIdx.x; it < a.nitems; it += gridDim.x, par ^= 1) {
             int c, m, n;
             item_mn(it, c, m, n);
             const unsigned* vm = a.vmax + (size_t)c * a.BEq;
-            const int gi = m * kI8Blk + rl;
+            const int gi = m * kI8Blk + rl, gjt = n * kI8Blk + rl;
             const unsigned vbi = gi < a.R ? vm[gi] : 0u;
+            const unsigned vbj = gjt < a.R ? vm[gjt] : 0u;
             const bool badi = !(__uint_as_float(vbi) <= 3.402823466e38f);
-            const int ei = i8_exponent(vbi);
+            const bool badj = !(__uint_as_float(vbj) <= 3.402823466e38f);
+            const double si = badi ? kNaN : pow2(i8_exponent(vbi) - 33);
+            colsc[par][rl] = badj ? kNaN : pow2(i8_exponent(vbj));
+            asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 epilogue warps
+            const double* sj = colsc[par];
             double* prow = a.part + ((size_t)c * a.BEp + gi) * a.BEp + (size_t)n * kI8Blk;
             // diagonal pairs carry the odd-j cross products once (see the MMA issuer): doubled here
             const double w1 = m == n ? 32768.0 : 16384.0, w3 = m == n ? 2.0 : 1.0;
@@ -427,18 +471,21 @@ __global__ void __launch_bounds__(kI8NT, 1)
                     for (int d = 0; d < kI8S; ++d) tmem_ld16_s32(t0 + 128 * d + j0, x[d]);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const int gj = n * kI8Blk + j0 + k;
-                        const unsigned vbj = gj < a.R ? __ldg(vm + gj) : 0u;
-                        const bool bad = badi || !(__uint_as_float(vbj) <= 3.402823466e38f);
+                    for (int k = 0; k < 16; k += 2) {
+                        double2 v;
                         // sum_i q_a q_b = 2^42 x0 + 2^35 x1 + 2^28 x2 + 2^21 x3 (each term exact in
-                        // fp64; the sum rounds once per term at 2^-53)
-                        const double sumq = (((double)x[0][k] * 2097152.0 + (double)x[1][k] * w1) +
-                                             (double)x[2][k] * 128.0) + (double)x[3][k] * w3;
-                        double v = bad ? __longlong_as_double(0x7ff8000000000000ULL)
-                                       : ldexp(sumq, ei + i8_exponent(vbj) - 54 + 21);
-                        if (kt0 > 0) v += prow[j0 + k];
-                        prow[j0 + k] = v;
+                        // fp64; the sum rounds once per term at 2^-53), in units of 2^21
+                        v.x = ((((double)x[0][k] * 2097152.0 + (double)x[1][k] * w1) + (double)x[2][k] * 128.0) +
+                               (double)x[3][k] * w3) * si * sj[j0 + k];
+                        v.y = ((((double)x[0][k + 1] * 2097152.0 + (double)x[1][k + 1] * w1) +
+                                (double)x[2][k + 1] * 128.0) + (double)x[3][k + 1] * w3) * si * sj[j0 + k + 1];
+                        double2* dst = reinterpret_cast<double2*>(prow + j0 + k);   // 16-byte aligned (BEp % 128 == 0)
+                        if (kt0 > 0) {
+                            const double2 o = *dst;
+                            v.x += o.x;
+                            v.y += o.y;
+                        }
+                        *dst = v;
                     }
                 }
                 tc_fence_before();

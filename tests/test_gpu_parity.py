@@ -522,6 +522,64 @@ def test_ab_switches_keep_parity(smf, torch, tmp_path, env):
     print(assert_parity(enh, alb, a_ref, r_ref, f"switch {env}"))
 
 
+_TAIL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2003_02978_b200 import smf, synth
+cols = int(sys.argv[3])
+cfg = synth.scaled(synth.CONFIGS["segment"], cols=cols, pixels=300, bands=13, rank=8)
+cube, s, _ = synth.generate(cfg)
+r = smf.Retriever(cfg.bands, s, n_iter=6)
+enh, alb, st = r.retrieve(torch.from_numpy(cube).cuda())
+torch.cuda.synchronize()
+assert int((st != 0).sum()) == 0
+np.save(sys.argv[2], np.stack([enh.cpu().numpy(), alb.cpu().numpy()]))
+"""
+
+
+def test_wide_tail_wave_split(smf, torch, tmp_path):
+    """Wide path with more columns than SMs: the last cols % SMs columns' k2w_init runs on a
+    second stream beside the other columns' statistics (DESIGN 5.6; the partitions are
+    independent). The tail columns and columns on either side of the split match the
+    oracle; SMF_TAIL_SPLIT=0 (one launch range) and =2 (the tail's statistics on the second
+    stream too) give the same bits; so does graph capture across the two streams."""
+    import os
+    import subprocess
+    import sys
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    cols = sms + 5
+    cfg = synth.scaled(synth.CONFIGS["segment"], cols=cols, pixels=300, bands=13, rank=8)
+    cube, s, _ = synth.generate(cfg)
+    enh, alb, st, *_ = run_gpu(smf, torch, cube, s, n_iter=6)
+    assert (st == 0).all()
+    for c in [0, sms - 1] + list(range(sms, cols)):
+        a_ref, r_ref, rc = oracle.retrieve_column(cube[c], s, n_iter=6)
+        assert rc == 0
+        print(assert_parity(enh[c:c + 1], alb[c:c + 1], a_ref[None], r_ref[None], f"tail split col {c}"))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for mode in ("0", "2"):
+        out = tmp_path / f"o{mode}.npy"
+        subprocess.run([sys.executable, "-c", _TAIL_SCRIPT, root, str(out), str(cols)], check=True, timeout=300,
+                       env={**os.environ, "SMF_TAIL_SPLIT": mode})
+        e2, a2 = np.load(out)
+        np.testing.assert_array_equal(e2, enh)
+        np.testing.assert_array_equal(a2, alb)
+    side = torch.cuda.Stream()
+    r = smf.Retriever(cfg.bands, s, n_iter=6, graph=True)
+    rad = torch.from_numpy(cube).cuda()
+    ws = r.alloc_workspace(cols, cfg.pixels)
+    eg = torch.empty((cols, cfg.pixels), device="cuda")
+    ag = torch.empty_like(eg)
+    sg = torch.empty(cols, dtype=torch.int32, device="cuda")
+    for _ in range(2):   # capture, replay
+        eg.fill_(-1.0)
+        with torch.cuda.stream(side):
+            r.retrieve(rad, eg, ag, ws, sg, stream=side)
+        side.synchronize()
+        np.testing.assert_array_equal(eg.cpu().numpy(), enh)
+        np.testing.assert_array_equal(ag.cpu().numpy(), alb)
+
+
 # ------------------------------------------------------------------ a2 error path: C^k + rho I at k >= 1
 @pytest.mark.parametrize("bands", [12, 13])
 def test_not_spd_after_signal_removal(smf, torch, bands):
