@@ -315,6 +315,9 @@ def main():
     # one process per GPU; with fewer visible GPUs than ranks (a plumbing test on one GPU,
     # never a measurement) ranks share devices round-robin and talk over gloo
     ndev = torch.cuda.device_count()
+    if ndev == 0:
+        sys.exit("bench.py: no CUDA device -- the product path has no CPU fallback "
+                 "(--impl reference times the oracle on the host)")
     local = local if local < ndev else local % ndev
     shared = world > ndev
     torch.cuda.set_device(local)
@@ -391,6 +394,8 @@ def main():
         ms = timed_steps()
     if world > 1:
         torch.distributed.barrier()
+    launches_per_step = r.last_launch_count   # of the timed region (the bracketed pass below launches the
+    #                                           wide statistics/init as one range: a few launches fewer)
     if not prof_in_timed:
         # per-kernel event brackets break the programmatic-dependent-launch overlap of
         # consecutive kernels, so the kernel durations come from a second, bracketed pass
@@ -399,7 +404,6 @@ def main():
         timed_steps()
     prof = r.profile_read()
     r.profile_enable(False)
-    launches_per_step = r.last_launch_count
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cpu" if shared else dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -485,6 +489,10 @@ def main():
                                                  + ("inside the timed region" if prof_in_timed else
                                                     "in a second pass of the same K steps right after "
                                                     "the (unbracketed) timed region")
+                                                 + ("; wide path: the bracketed launches run k2w_init as one column "
+                                                    "range (the timed region hides its partial last wave on a second "
+                                                    "stream, DESIGN 5.6), so k2_init here exceeds its share of the step"
+                                                    if not (cfg.bands <= 96 and cfg.bands % 4 == 0) else "")
                                                  + (f"; rank 0's {ncols}-column share" if world > 1 else "")},
                 "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk.summary(),

@@ -21,9 +21,12 @@
 //             int8 slice cube [cols][4][R = B + 2][Np] (transposed through shared memory)
 //  k1w_syrk_i8  persistent; a work item = (column, 128 x 128 row-block pair m >= n); TMA
 //             loads the 4 (diagonal) or 8 slice tiles of 128 rows x 64 pixels per K tile
-//             (SWIZZLE_64B); one thread issues the 10 (diagonal pairs: 7) kind::i8 MMAs per 32-pixel K step into
-//             four int32 TMEM accumulators (all 512 columns); 4 epilogue warps combine them in
-//             fp64 into the column's [BEp][BEp] partial that k2w_init consumes.
+//             (SWIZZLE_64B); one thread issues the 10 (diagonal pairs: 7) digit products per
+//             32-pixel K step as 6 (4) kind::i8 MMAs -- two products per N = 256 instruction
+//             where they fill adjacent accumulators -- into four int32 TMEM accumulators (all
+//             512 columns); 4 epilogue warps combine them in fp64
+//             (exact power-of-two scales)
+//             into the column's [BEp][BEp] partial that k2w_init consumes.
 #pragma once
 #include <cstdint>
 
@@ -36,7 +39,11 @@ constexpr int kI8S = 4;            // digits (slices) per value
 constexpr int kI8Tile = 64;        // pixels per K tile (one 64-byte swizzle row per band row)
 constexpr int kI8QTile = 128;      // pixels per k1w_quant block
 constexpr int kI8Stages = 3;       // TMA ring depth of the SYRK
-constexpr int kI8NT = 192;         // SYRK threads: TMA warp, MMA warp, 4 epilogue warps
+#ifndef SMF_I8_EPIW
+#define SMF_I8_EPIW 4              // epilogue warps: 4, or 8 (two per TMEM lane quadrant, 64 columns each; measured equal)
+#endif
+constexpr int kI8EpiW = SMF_I8_EPIW;
+constexpr int kI8NT = 64 + 32 * kI8EpiW;   // SYRK threads: TMA warp, MMA warp, the epilogue warps
 constexpr int kI8MaxRun = 2048;    // K tiles per int32 run (131072 pixels: 4 digit products <= 4 * 64^2 per pixel)
 constexpr uint32_t kI8TileBytes = kI8Blk * kI8Tile;   // one slice of one block: 8 KB
 constexpr int kI8ScanPix = 128;    // pixels per k1w_scan block
@@ -322,7 +329,7 @@ __global__ void __launch_bounds__(kI8NT, 1)
             mbar_init(&empty[s], 1);
         }
         mbar_init(&acc_full, 1);
-        mbar_init(&acc_empty, 4);
+        mbar_init(&acc_empty, kI8EpiW);
         fence_mbar_init();
     }
     if (wid == 1) tmem_alloc(&tmem_sh, 512);
@@ -440,6 +447,8 @@ __global__ void __launch_bounds__(kI8NT, 1)
         // single-buffered: all 512 TMEM columns hold one item).
         const int q = wid & 3;                 // TMEM lane quadrant this warp may access
         const int rl = 32 * q + lane;          // row within the block
+        const int half = (wid - 2) >> 2;       // column half of this warp (8 epilogue warps)
+        constexpr int kColsW = kI8Blk * 4 / kI8EpiW;   // columns per warp: 128 or 64
         const double kNaN = __longlong_as_double(0x7ff8000000000000ULL);
         auto pow2 = [](int e) { return __longlong_as_double((long long)(e + 1023) << 52); };   // -1022 <= e <= 1023
         uint32_t runs = 0;
@@ -454,8 +463,8 @@ __global__ void __launch_bounds__(kI8NT, 1)
             const bool badi = !(__uint_as_float(vbi) <= 3.402823466e38f);
             const bool badj = !(__uint_as_float(vbj) <= 3.402823466e38f);
             const double si = badi ? kNaN : pow2(i8_exponent(vbi) - 33);
-            colsc[par][rl] = badj ? kNaN : pow2(i8_exponent(vbj));
-            asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 epilogue warps
+            if (half == 0) colsc[par][rl] = badj ? kNaN : pow2(i8_exponent(vbj));
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kI8EpiW) : "memory");   // the epilogue warps
             const double* sj = colsc[par];
             double* prow = a.part + ((size_t)c * a.BEp + gi) * a.BEp + (size_t)n * kI8Blk;
             // diagonal pairs carry the odd-j cross products once (see the MMA issuer): doubled here
@@ -465,7 +474,7 @@ __global__ void __launch_bounds__(kI8NT, 1)
                 tc_fence_after();
                 const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16);
 #pragma unroll 1
-                for (int j0 = 0; j0 < kI8Blk; j0 += 16) {
+                for (int j0 = half * kColsW; j0 < (half + 1) * kColsW; j0 += 16) {
                     int x[kI8S][16];
 #pragma unroll
                     for (int d = 0; d < kI8S; ++d) tmem_ld16_s32(t0 + 128 * d + j0, x[d]);
