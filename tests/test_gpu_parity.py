@@ -785,11 +785,14 @@ def test_literal_iteration_grouped_and_masked(smf, torch, bands):
                             f"literal grouped+masked B={bands} {c0}:{c1}"))
 
 
-def test_wide_int8_statistics_multi_run_partition(smf, torch):
+@pytest.mark.parametrize("bands", [13, 130])
+def test_wide_int8_statistics_multi_run_partition(smf, torch, bands):
     """A pooled wide partition longer than one int32 run of the int8 SYRK (131 072 pixels:
     the digit products' overflow bound) -- the runs are folded into the fp64 partial
-    (all-columns grouping). C0 against the oracle on the pooled rows, and parity."""
-    cols, pixels, bands = 3, 50000, 13
+    (all-columns grouping). C0 against the oracle on the pooled rows, and parity.
+    130 bands: two row blocks, the second a 16-row compact operand (the transposed 'thin'
+    block pairs fold their runs too)."""
+    cols, pixels = 3, 50000
     cfg = synth.scaled(synth.CONFIGS["tiny"], cols=cols, pixels=pixels, bands=bands, rank=8)
     cube, s, _ = synth.generate(cfg)
     pooled = cube.reshape(1, cols * pixels, bands)
