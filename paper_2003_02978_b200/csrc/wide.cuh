@@ -421,11 +421,12 @@ __global__ void __launch_bounds__(kWideNTI, 1) k2w_init(WideInitArgs a) {
 // ---------------------------------------------------------------- K2w update
 // shared: t [B], x_f [2][B] (forward: t, h -> L^-1 t, L^-1 h), with the energy trace x_b [4][B]
 // (backward right-hand sides; otherwise the one backward right-hand side replaces w_t in x_f),
-// yv [4][32], scratch [96], then (128-byte aligned) the factor ring [kTsS][32][32] of the
-// streamed solves (wide_chol.cuh; 44.9 KB in all at B = 425: five CTAs per SM), which the
+// yv [4][32], scratch [96], then (128-byte aligned) the factor ring [kTsS][kTsT][32][32] of the
+// streamed solves (wide_chol.cuh; 2 stages of 2 tiles: 44.9 KB in all at B = 425, five CTAs per
+// SM), which the
 // literal path reuses as the diagonal block [32][33] and reduction [4][2][32] of tri_fwd
 __host__ inline size_t k2w_update_smem(int B, int energy) {
-    return (size_t)((energy ? 7 : 3) * B + 4 * 32 + 96 + 16 + kTsS * kTileD) * 8;
+    return (size_t)((energy ? 7 : 3) * B + 4 * 32 + 96 + 16 + kTsS * kStageD) * 8;
 }
 constexpr int kLitRows = 32;   // residual rows per chunk of the wide literal check
 // doubles of global scratch per column for the wide literal check (packed C^k + residual rows)

@@ -358,21 +358,31 @@ __device__ void tri_bwd(const double* __restrict__ M, int B, double* x, double* 
 // butterfly reduce-scatter.
 constexpr int kTileD = kChB * kChB;   // doubles per factor tile
 #ifndef SMF_K2W_STAGES
-#define SMF_K2W_STAGES 3
+#define SMF_K2W_STAGES 2
 #endif
 constexpr int kTsS = SMF_K2W_STAGES;  // ring depth (k2w_update: five CTAs per SM at B = 425)
+// Tiles per stage: the kernel is bound by each warp's instruction latency chain (an mbarrier
+// wait, a release and the ring bookkeeping per stage), not by bytes in flight, so a stage holds
+// two adjacent off-diagonal tiles of a row block (the last one of an odd count and the
+// diagonal tile travel alone): 63 instead of 105 stages per pass at B = 425 for the same
+// 32 KB ring as four one-tile stages.
+#ifndef SMF_K2W_PAIR
+#define SMF_K2W_PAIR 1
+#endif
+constexpr int kTsT = SMF_K2W_PAIR ? 2 : 1;
+constexpr int kStageD = kTsT * kTileD;   // doubles per stage
 
 // Stage index / phase bookkeeping is incremental (no divisions) and the issuing thread walks
 // the tile order with a cursor (no triangular decode): thread 0 is also a consumer, so every
 // cycle it spends issuing is on warp 0's path.
 struct TileStream {
-    double* ring;          // [kTsS][32][32] shared, 128-byte aligned
+    double* ring;          // [kTsS][kTsT][32][32] shared, 128-byte aligned
     uint64_t* full;        // [kTsS] TMA completion
     uint64_t* empty;       // [kTsS] one arrival per warp
     const CUtensorMap* map;
     int nblk, col;
-    int total;             // tiles in the whole sequence (forward + backward)
-    int consumed;          // every thread: tiles consumed (program order)
+    int total;             // stages in the whole sequence (forward + backward)
+    int consumed;          // every thread: stages consumed (program order)
     int cs, cph;           // every thread: stage and full-barrier phase of the next tile to consume
     // thread 0 (issuer): tiles issued, stage / empty phase of the next issue, tile cursor
     int issued, ps, pph, pI, pJ, pfwd;
@@ -386,7 +396,9 @@ __device__ __forceinline__ void ts_init(TileStream& ts, double* ring, uint64_t* 
     ts.map = map;
     ts.nblk = (B + kChB - 1) / kChB;
     ts.col = col;
-    ts.total = npass * ts.nblk * (ts.nblk + 1) / 2;
+    int per_pass = 0;   // a row block with n off-diagonal tiles: ceil(n / kTsT) stages + the diagonal's
+    for (int n = 0; n < ts.nblk; ++n) per_pass += (n + kTsT - 1) / kTsT + 1;
+    ts.total = npass * per_pass;
     ts.consumed = 0;
     ts.cs = 0;
     ts.cph = 0;
@@ -413,8 +425,16 @@ __device__ __forceinline__ void ts_issue(TileStream& ts, int upto) {
             mbar_wait(&ts.empty[ts.ps], (uint32_t)ts.pph);   // the stage's previous tile released
             fence_proxy_async();   // the warps' generic reads of the stage before the async refill
         }
-        mbar_arrive_expect_tx(&ts.full[ts.ps], kTileD * 8);
-        tma_load_3d(ts.ring + (size_t)ts.ps * kTileD, ts.map, &ts.full[ts.ps], ts.pJ * kChB, ts.pI * kChB, ts.col);
+        // an off-diagonal tile takes the row block's next off-diagonal tile along
+        const int Jn = ts.pfwd ? ts.pJ + 1 : ts.pJ - 1;
+        const bool two = kTsT == 2 && ts.pJ != ts.pI && Jn != ts.pI;
+        double* dst = ts.ring + (size_t)ts.ps * kStageD;
+        mbar_arrive_expect_tx(&ts.full[ts.ps], (two ? 2 : 1) * kTileD * 8);
+        tma_load_3d(dst, ts.map, &ts.full[ts.ps], ts.pJ * kChB, ts.pI * kChB, ts.col);
+        if (two) {
+            tma_load_3d(dst + kTileD, ts.map, &ts.full[ts.ps], Jn * kChB, ts.pI * kChB, ts.col);
+            ts.pJ = Jn;   // the cursor step below then leaves the pair
+        }
         ++ts.issued;
         if (++ts.ps == kTsS) {
             ts.ps = 0;
@@ -438,7 +458,7 @@ __device__ __forceinline__ void ts_issue(TileStream& ts, int upto) {
 __device__ __forceinline__ const double* ts_acquire(TileStream& ts) {
     if (threadIdx.x == 0) ts_issue(ts, ts.consumed + kTsS);
     mbar_wait(&ts.full[ts.cs], (uint32_t)ts.cph);
-    return ts.ring + (size_t)ts.cs * kTileD;
+    return ts.ring + (size_t)ts.cs * kStageD;
 }
 
 __device__ __forceinline__ void ts_release(TileStream& ts) {
@@ -509,18 +529,31 @@ __device__ __forceinline__ void tri_stream(TileStream& ts, int B, double* x, dou
 #pragma unroll
         for (int e = 0; e < V; ++e) acc[e] = 0.0;
         const int nJ = FWD ? I : nblk - 1 - I;   // off-diagonal tiles of the row block
-        for (int jj = 0; jj < nJ; ++jj) {
+        for (int jj = 0; jj < nJ; jj += kTsT) {
             const int J = FWD ? jj : nblk - 1 - jj;
             const int cJ = J * kChB + lane;
-            double xv[NR];
+            const bool two = kTsT == 2 && jj + 1 < nJ;   // the stage holds tile J and the next one (block-uniform)
+            const int cJ2 = cJ + (FWD ? kChB : -kChB);
+            double xv[NR], xv2[NR];
 #pragma unroll
-            for (int q = 0; q < NR; ++q) xv[q] = cJ < B ? x[q * B + cJ] : 0.0;
+            for (int q = 0; q < NR; ++q) {
+                xv[q] = cJ < B ? x[q * B + cJ] : 0.0;
+                xv2[q] = (two && cJ2 < B) ? x[q * B + cJ2] : 0.0;
+            }
             const double* T = ts_acquire(ts);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const double l = T[(r0 + i) * kChB + lane];
 #pragma unroll
                 for (int q = 0; q < NR; ++q) acc[i * NR + q] = fma(l, xv[q], acc[i * NR + q]);
+            }
+            if (two) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const double l = T[kTileD + (r0 + i) * kChB + lane];
+#pragma unroll
+                    for (int q = 0; q < NR; ++q) acc[i * NR + q] = fma(l, xv2[q], acc[i * NR + q]);
+                }
             }
             ts_release(ts);
         }
