@@ -119,7 +119,12 @@ int smf_supported_bands(int bands);
  *   albedo        device fp32 [cols][pixels] out: raw r_i (Eq. 7), 1 if albedo off
  *   workspace     device, >= smf_workspace_bytes(cols, pixels), 256-byte aligned
  *   column_status device int32 [cols] out, or NULL
- * enhancement and albedo must not alias each other or the radiance. */
+ * enhancement and albedo must not alias each other or the radiance.
+ * Ordering: everything is ordered after the work already in `stream` and complete when
+ * `stream` reaches the point after this call. On the wide path with more columns than SMs the
+ * initial factorisation of the last cols mod SMs columns (independent partitions)
+ * runs on a second stream the context owns, forked from and joined back into `stream` by
+ * events inside this call -- a caller only ever synchronises with `stream`. */
 smf_status smf_retrieve(smf_ctx* ctx, const float* radiance, int cols, int pixels,
                         float* enhancement, float* albedo, void* workspace,
                         int32_t* column_status, void* stream);
